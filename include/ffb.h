@@ -1,0 +1,168 @@
+/* libffb — C-ABI of the B200-native FlipFlop analysis path.
+ *
+ * The reference (pkg/src/ptxwatt, pure Python) has no FFI of its own; its boundary is the
+ * Python API re-exported at pkg/src/ptxwatt/__init__.py:4-55.  Each entry point below
+ * names the reference function(s) it stands in for.  The Python shim in
+ * paper_2601_13345_b200/ binds these with ctypes (see INTEGRATION.md for the stub a
+ * maintainer of the reference would add).
+ *
+ * Conventions
+ *  - every function returns an int32 status (FFB_OK or FFB_E_*); FFB_E_* values map 1:1
+ *    onto the reference's exception classes (pkg/src/ptxwatt/errors.py), see
+ *    paper_2601_13345_b200/errors.py:STATUS_TABLE;
+ *  - pointers named d_* are DEVICE pointers owned by the caller, h_* are HOST pointers;
+ *    nothing is allocated that the caller must free except the context;
+ *  - every launch goes to the cudaStream_t passed in (void* here so the header is plain C);
+ *    functions do not synchronise unless documented ("syncs");
+ *  - all functions are reentrant across contexts; one context serves one device and is
+ *    not thread-safe by itself.
+ */
+#ifndef FFB_H_
+#define FFB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFB_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------------------ */
+enum {
+  FFB_OK = 0,
+  FFB_E_MALFORMED_PTX = 1,   /* errors.py MalformedPtx  (ptx.py:175,184,273,275,281)     */
+  FFB_E_NO_KERNEL = 2,       /* errors.py NoKernelFound (ptx.py:186-187)                 */
+  FFB_E_INVALID_CONFIG = 3,  /* errors.py InvalidConfig (features.py:98,102)             */
+  FFB_E_NO_FEASIBLE = 4,     /* errors.py NoFeasibleConfig (explorer.py:146,207)         */
+  FFB_E_EMPTY_GRID = 5,      /* errors.py EmptyGrid (time_model.py:76, power_model.py:85)*/
+  FFB_E_ZERO_DELAY = 6,      /* errors.py ZeroDelay (time_model.py:36)                   */
+  FFB_E_ZERO_COMPUTE = 7,    /* errors.py ZeroComputeCycles (time_model.py:43)           */
+  FFB_E_ZERO_BANDWIDTH = 8,  /* errors.py ZeroBandwidth (time_model.py:110)              */
+  FFB_E_ZERO_CYCLES = 9,     /* errors.py ZeroCycles (power_model.py:36)                 */
+  FFB_E_CAP_ABOVE_TDP = 10,  /* errors.py CapAboveTdp (power_model.py:100-105)           */
+  FFB_E_CAPACITY = 11,       /* a documented device capacity was exceeded                */
+  FFB_E_CUDA = 12,           /* CUDA runtime failure; see ffb_last_error                 */
+  FFB_E_BAD_ARGUMENT = 13
+};
+
+/* ---- opcode classes / state spaces (ptx.py:15-16) ------------------------------------ */
+enum { FFB_CLS_MEMLOAD = 0, FFB_CLS_MEMSTORE, FFB_CLS_FP32, FFB_CLS_INT, FFB_CLS_SFU,
+       FFB_CLS_ALU, FFB_CLS_SYNC, FFB_CLS_BRANCH, FFB_CLS_OTHER, FFB_N_CLASSES };
+enum { FFB_SP_GLOBAL = 0, FFB_SP_SHARED, FFB_SP_LOCAL, FFB_SP_PARAM, FFB_SP_REG, FFB_SP_NONE };
+
+/* ---- per-kernel feature row: features.py:62-81 + alignment.py:128-147 ---------------- */
+enum { FFB_F_N_MEM = 0, FFB_F_MEM_BYTES, FFB_F_FP32, FFB_F_INT, FFB_F_SFU, FFB_F_ALU,
+       FFB_F_N_SYNC, FFB_F_ALIGNED, FFB_F_STATIC_SHARED, FFB_F_REGS_DECLARED,
+       FFB_F_N_INSTR, FFB_F_RESERVED,
+       /* Override columns, used by the single-point drop-ins (predict_energy, execution_time,
+        * dynamic_power) whose KernelFeatures argument carries its own occupancy numbers:
+        * when FFB_F_OVR != 0 the kernel takes warps / blocks_per_sm / eta / n_comp from the
+        * row instead of deriving them, and FFB_F_OVR_TEXEC (if not NaN) replaces t_exec in the
+        * transient test of power_model.py:93-95. */
+       FFB_F_OVR, FFB_F_OVR_WARPS, FFB_F_OVR_BPS, FFB_F_OVR_ETA, FFB_F_OVR_NCOMP, FFB_F_OVR_TEXEC,
+       FFB_FEAT_WIDTH };
+
+/* ---- one GPU spec + calibration, flattened (calibration.py:43-83) -------------------- */
+enum FfbSpecCol {
+  FFB_S_SM_COUNT = 0, FFB_S_MAX_WARPS, FFB_S_MAX_SHARED, FFB_S_MAX_THREADS,
+  FFB_S_BW_MAX, FFB_S_IPC, FFB_S_F_BASE, FFB_S_P_TDP, FFB_S_P_STATIC, FFB_S_P_CAP_MIN,
+  FFB_S_DVFS_K, FFB_S_TAU_SHORT, FFB_S_DEP_DELAY, FFB_S_T_BARRIER,
+  FFB_S_EXEC0, FFB_S_ISSUE0 = FFB_S_EXEC0 + 5, FFB_S_BETA0 = FFB_S_ISSUE0 + 5, /* FP32,INT,SFU,ALU,Mem */
+  FFB_S_L_COAL = FFB_S_BETA0 + 5, FFB_S_L_UNCOAL, FFB_S_SM_ALPHA, FFB_S_SM_BETA, FFB_S_SM_DELTA,
+  FFB_S_TRANSIENT_R, FFB_S_KAPPA, FFB_S_LAMBDA, FFB_S_P_BASE_SHAPE, FFB_S_P_MEM_BASE,
+  FFB_S_W_MEM, FFB_S_W_COMP, FFB_S_W_SYNC, FFB_S_T_BASE, FFB_S_E_OVERHEAD,
+  FFB_S_REGS_PER_SM,   /* extension: 0 = no register limit (reference behaviour) */
+  FFB_SPEC_USED,
+  FFB_SPEC_WIDTH = 48
+};
+
+/* ---- detail row written by ffb_predict_grid when d_detail != NULL --------------------
+ * time_model.py:20-30 TimeBreakdown, power_model.py:16-28 PowerBreakdown, plus occupancy. */
+enum { FFB_D_MWP = 0, FFB_D_CWP, FFB_D_BW_EFF, FFB_D_T_MEM, FFB_D_T_COMP, FFB_D_T_SYNC, FFB_D_T_EXEC,
+       FFB_D_P_UNITS, FFB_D_P_SHAPE, FFB_D_P_MEM, FFB_D_P_SM, FFB_D_P_DYN, FFB_D_F_ADJ, FFB_D_CI,
+       FFB_D_ACTIVE_SMS, FFB_D_CAP_LIMITED, FFB_D_E_PRED, FFB_D_WARPS, FFB_D_BLOCKS_PER_SM,
+       FFB_D_ETA, FFB_DETAIL_WIDTH };
+
+/* flag bits of d_flags */
+enum { FFB_PT_VALID = 1, FFB_PT_CAP_LIMITED = 2 };
+
+typedef struct FfbContext FfbContext;
+
+int32_t ffb_abi_version(void);
+/* One context per device.  Allocates small scratch (tables, counters) on `device`. */
+int32_t ffb_create(int32_t device, FfbContext** out);
+int32_t ffb_destroy(FfbContext* ctx);
+/* Text of the last failure on this context (never NULL). */
+const char* ffb_last_error(const FfbContext* ctx);
+/* Number of kernels this context has launched so far (bench.py's gpu_launches). */
+int64_t ffb_launch_count(const FfbContext* ctx);
+
+/* ---- K2 + K3: occupancy filter and fp64 time / power / energy over the grid ----------
+ * Stands in for explorer.py:59-94 (generate_valid_configs: the validity mask),
+ * features.py:96-114 (occupancy), features.py:55-59 (eta), time_model.py:67-129,
+ * power_model.py:109-170 and explorer.py:97-108 (energy identity), evaluated for every
+ * point of   kernel k  x  spec s  x  shape j  x  cap c,   output index ((k*S+s)*J+j)*C+c.
+ *
+ * libm log/pow (power_model.py:61,76,106) are taken on the HOST inside this call with the
+ * same libm CPython uses and uploaded as tables, so results are bit-identical to the
+ * reference; the device code uses only IEEE +,-,*,/ without FMA contraction.
+ * Invalid points (explorer.py:79-91 rules) get t = e = +inf and flag bit FFB_PT_VALID clear.
+ */
+typedef struct {
+  int64_t n_kernels, n_specs, n_shapes, n_caps;
+  const double*  d_feat;    /* [K, FFB_FEAT_WIDTH]                                         */
+  const int64_t* d_res;     /* [K, 2] {dynamic shared bytes, total blocks}  (launch.py:24) */
+  const double*  h_spec;    /* [S, FFB_SPEC_WIDTH]                                         */
+  const int32_t* h_shape;   /* [J, 4] {block_x, block_y, block_z, regs_per_thread}         */
+  const double*  h_cap;     /* [C] watts                                                   */
+  double*  d_t;             /* [K,S,J,C] t_exec, or NULL                                   */
+  double*  d_e;             /* [K,S,J,C] e_pred, or NULL                                   */
+  double*  d_pdyn;          /* [K,S,J,C] or NULL                                           */
+  uint8_t* d_flags;         /* [K,S,J,C] or NULL                                           */
+  double*  d_occ;           /* [K,S,J]   blocks_per_sm (features.py:114), or NULL          */
+  double*  d_detail;        /* [K,S,J,C,FFB_DETAIL_WIDTH] or NULL                          */
+  uint32_t* d_status;       /* [1] OR-ed bit (1<<FFB_E_*) of model errors met, or NULL      */
+  int32_t strict;           /* 1: no validity masking, reference exceptions are reported
+                                  in d_status (predict_energy / extract_features semantics) */
+} FfbGridDesc;
+int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void* stream);
+
+/* Shapes that pass explorer.py:76-88 for one spec and one dynamic-shared size, in the
+ * canonical (threads, bx, by) order of explorer.py:55-56,93.  Host-side integer work;
+ * writes up to cap_shapes {bx,by} pairs, returns the count in *n_out. */
+int32_t ffb_enumerate_shapes(const double* h_spec_row, int64_t shared_dyn,
+                             const int32_t* h_dims, int64_t n_dims,
+                             int32_t* h_out_xy, int64_t cap_shapes, int64_t* n_out);
+
+/* ---- K4: skyline ----------------------------------------------------------------------
+ * explorer.py:122-140 (pareto_front), :209-212 (throughput floor + ordering).
+ * A point is dropped iff some point has strictly lower e AND strictly lower t; ties stay.
+ *
+ * Segmented form: n_groups consecutive groups of group_size points.  For each group:
+ *   t_peak = min t;  eligible = t <= t_peak / rho  (rho <= 0 disables the floor);
+ *   front of the eligible points, written as in-group indices ordered by
+ *   (e, t, tie[idx]) — pass tie = rank of (block_x, block_y, cap) to reproduce
+ *   explorer.py:113-119; NULL means the index itself.
+ * d_front_idx [n_groups, cap_front]; d_front_n [n_groups] (true size, even if > cap_front,
+ * in which case the status word gets FFB_E_CAPACITY); d_tpeak [n_groups] or NULL.
+ */
+int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const double* d_t,
+                           int64_t n_groups, int64_t group_size, const uint32_t* d_tie,
+                           double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
+                           double* d_tpeak, int64_t cap_front, uint32_t* d_status, void* stream);
+
+/* One large candidate set (BASELINE config 5).  Streaming cull against a sentinel
+ * staircase, exact pass on the survivors.  Output: global indices (or d_id values when
+ * d_id != NULL) of the front in (e, t, id) order.  Syncs (returns the count).
+ * d_occ != NULL switches to the 3-objective rule (maximise occupancy as third key):
+ * dropped iff some point is strictly better in all three. */
+int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double* d_t, const double* d_occ,
+                    const uint64_t* d_id, int64_t n, double rho, uint64_t* d_front_id,
+                    double* d_front_e, double* d_front_t, int64_t cap_front,
+                    int64_t* h_front_n, double* h_tpeak, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFB_H_ */

@@ -1,0 +1,454 @@
+// K4: Pareto skyline in (energy, time).
+//
+// Reference rule restated (explorer.py:122-140, :209-212): after the throughput floor
+// t <= t_peak / rho, a point is dropped iff another point has STRICTLY lower e and
+// STRICTLY lower t; equal points and partial ties all stay; the front is reported in
+// (e, t, tie) order where tie reproduces the reference's (block_x, block_y, p_cap) key.
+//
+// One CTA owns one group of candidates:
+//   1. stream the group's (e, t) from HBM into shared memory (the only DRAM traffic:
+//      16 B per candidate), reducing min t on the way;
+//   2. floor, then a 256-bucket histogram of min-t over the e range and its exclusive
+//      prefix-min: a point whose lower-e buckets already hold a smaller t is provably
+//      dominated (buckets are monotone in e, so "lower bucket" implies "strictly lower e");
+//   3. the few survivors (every true front member survives) are bitonic-sorted by the
+//      reference key and filtered exactly with a prefix-min over strictly-lower-e groups,
+//      evaluated with warp-shuffle scans — the sort-based skyline of north_star (4).
+// Large single sets (BASELINE config 5) reuse the same kernel hierarchically: fronts of
+// 4096-point chunks are appended to a compact buffer and reduced again until one group is
+// left; exact because strict dominance is transitive.
+#include "ffb_common.cuh"
+
+#include <math.h>
+#include <string.h>
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBuckets = 256;
+constexpr uint32_t kPad = 0xffffffffu;
+
+FFB_HD uint64_t ordered_bits(double v) {
+  // monotone map double -> uint64 (total order on non-NaN values)
+#if defined(__CUDA_ARCH__) || defined(FFB_SIMT_EMUL)
+  uint64_t b = (uint64_t)__double_as_longlong(v);
+#else
+  uint64_t b; memcpy(&b, &v, 8);
+#endif
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+struct SkyArgs {
+  const double* e;
+  const double* t;
+  const uint64_t* id;       // optional per-point id (tie-break + compact output)
+  const uint32_t* tie;      // optional [group_size] tie rank
+  int64_t n_total;          // total points (last group may be short)
+  int64_t group_size;
+  double rho;               // <= 0: no floor
+  int resident;             // points staged in shared memory
+  int surv_cap;             // survivor capacity (power of two)
+  // per-group outputs (optional)
+  uint32_t* front_idx;
+  uint32_t* front_n;
+  double* tpeak;
+  int64_t cap_front;
+  // compact outputs (optional): appended at an atomically reserved offset
+  double* out_e;
+  double* out_t;
+  uint64_t* out_id;
+  unsigned long long* out_count;
+  int64_t out_cap;
+  uint32_t* status;
+};
+
+template <typename T, typename Op>
+FFB_D T warp_scan_incl(T v, Op op, T ident) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v = op(v, o);
+  }
+  (void)ident;
+  return v;
+}
+
+// In-place inclusive scan of arr[0..n) by the whole CTA. part: kThreads scratch entries.
+template <typename T, typename Op>
+FFB_D void block_scan_incl(T* arr, int n, T* part, Op op, T ident) {
+  const int tid = threadIdx.x;
+  const int per = (n + kThreads - 1) / kThreads;
+  const int lo = tid * per;
+  const int hi = lo + per < n ? lo + per : n;
+  T acc = ident;
+  for (int i = lo; i < hi; ++i) { acc = op(acc, arr[i]); arr[i] = acc; }
+  T incl = warp_scan_incl(acc, op, ident);
+  const int lane = tid & 31, wid = tid >> 5;
+  if (lane == 31) part[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < kThreads / 32 ? part[lane] : ident;
+    w = warp_scan_incl(w, op, ident);
+    if (lane < kThreads / 32) part[lane] = w;
+  }
+  __syncthreads();
+  T excl_lane = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl_lane = ident;
+  T prefix = op(wid > 0 ? part[wid - 1] : ident, excl_lane);
+  for (int i = lo; i < hi; ++i) arr[i] = op(prefix, arr[i]);
+  __syncthreads();
+}
+
+struct MinD { FFB_D double operator()(double a, double b) const { return b < a ? b : a; } };
+struct MaxU { FFB_D uint32_t operator()(uint32_t a, uint32_t b) const { return b > a ? b : a; } };
+struct AddU { FFB_D uint32_t operator()(uint32_t a, uint32_t b) const { return a + b; } };
+
+FFB_D double block_reduce_min(double v, double* part) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) { double o = __shfl_xor_sync(0xffffffffu, v, d); v = o < v ? o : v; }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) part[wid] = v;
+  __syncthreads();
+  double r = part[0];
+  for (int w = 1; w < kThreads / 32; ++w) r = part[w] < r ? part[w] : r;
+  return r;
+}
+FFB_D double block_reduce_max(double v, double* part) { return -block_reduce_min(-v, part); }
+
+__global__ void __launch_bounds__(kThreads)
+skyline_group_kernel(SkyArgs a) {
+  FFB_DYN_SMEM(smem_raw);
+  __shared__ double s_part[kThreads / 32 + 1];
+  __shared__ unsigned long long s_bmin[kBuckets];
+  __shared__ unsigned int s_count;
+  __shared__ unsigned long long s_base;
+
+  const int tid = threadIdx.x;
+  const int64_t g = blockIdx.x;
+  const int64_t p0 = g * a.group_size;
+  int64_t rem = a.n_total - p0;
+  const int G = (int)(rem < a.group_size ? rem : a.group_size);
+  const int MC = a.surv_cap;
+
+  // shared-memory carve-up: [resident e,t] [sv_idx MC] [pm MC] [gs MC]
+  double* s_e = reinterpret_cast<double*>(smem_raw);
+  double* s_t = s_e + (a.resident ? a.group_size : 0);
+  double* s_pm = s_t + (a.resident ? a.group_size : 0);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_pm + MC);
+  uint32_t* s_gs = s_idx + MC;
+
+  const double* ge = a.e + p0;
+  const double* gt = a.t + p0;
+  const double* pe = a.resident ? s_e : ge;
+  const double* pt = a.resident ? s_t : gt;
+
+  // ---- 1. load + min t ----
+  double tmin = INFINITY;
+  for (int i = tid; i < G; i += kThreads) {
+    const double tv = gt[i];
+    if (a.resident) { s_e[i] = ge[i]; s_t[i] = tv; }
+    tmin = tv < tmin ? tv : tmin;
+  }
+  const double t_peak = block_reduce_min(tmin, s_part);
+  if (tid == 0) { s_count = 0; if (a.tpeak) a.tpeak[g] = t_peak; }
+  const double thr = (a.rho > 0.0) ? t_peak / a.rho : INFINITY;       // explorer.py:210
+  // ---- 2. e range over eligible points ----
+  double emin = INFINITY, emax = -INFINITY;
+  for (int i = tid; i < G; i += kThreads) {
+    const double ev = pe[i], tv = pt[i];
+    const bool ok = tv <= thr && ev < INFINITY && tv < INFINITY;
+    if (ok) { emin = ev < emin ? ev : emin; emax = ev > emax ? ev : emax; }
+  }
+  emin = block_reduce_min(emin, s_part);
+  emax = block_reduce_max(emax, s_part);
+  for (int b = tid; b < kBuckets; b += kThreads) s_bmin[b] = ~0ull;
+  __syncthreads();
+  const double span = emax - emin;
+  const double scale = (span > 0.0 && span < INFINITY) ? (double)(kBuckets - 1) / span : 0.0;
+  // ---- 3. bucket min-t ----
+  for (int i = tid; i < G; i += kThreads) {
+    const double ev = pe[i], tv = pt[i];
+    const bool ok = tv <= thr && ev < INFINITY && tv < INFINITY;
+    if (ok) {
+      int b = (int)((ev - emin) * scale);
+      b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
+      atomicMin(&s_bmin[b], (unsigned long long)ordered_bits(tv));
+    }
+  }
+  __syncthreads();
+  // exclusive prefix-min over buckets (kThreads == kBuckets)
+  {
+    unsigned long long v = s_bmin[tid];
+    unsigned long long incl = v;
+    const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      unsigned long long o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl = o < incl ? o : incl;
+    }
+    unsigned long long* wpart = reinterpret_cast<unsigned long long*>(s_part);
+    __syncthreads();
+    if (lane == 31) wpart[wid] = incl;
+    __syncthreads();
+    unsigned long long before = ~0ull;
+    for (int w = 0; w < wid; ++w) before = wpart[w] < before ? wpart[w] : before;
+    unsigned long long excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = ~0ull;
+    excl = before < excl ? before : excl;
+    __syncthreads();
+    s_bmin[tid] = excl;
+  }
+  __syncthreads();
+  // ---- 4. cull, collect survivors ----
+  for (int i0 = 0; i0 < G; i0 += kThreads) {
+    const int i = i0 + tid;
+    bool keep = false;
+    if (i < G) {
+      const double ev = pe[i], tv = pt[i];
+      const bool ok = tv <= thr && ev < INFINITY && tv < INFINITY;
+      if (ok) {
+        int b = (int)((ev - emin) * scale);
+        b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
+        keep = !(s_bmin[b] < (unsigned long long)ordered_bits(tv));
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int lane = tid & 31;
+    unsigned base = 0;
+    if (lane == 0 && m) base = atomicAdd(&s_count, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+      if (pos < (unsigned)MC) s_idx[pos] = (uint32_t)i;
+    }
+  }
+  __syncthreads();
+  const unsigned m_surv = s_count;
+  if (m_surv > (unsigned)MC) {
+    if (tid == 0) {
+      if (a.front_n) a.front_n[g] = kPad;
+      if (a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
+    }
+    return;
+  }
+  int m2 = 1;
+  while (m2 < (int)m_surv) m2 <<= 1;
+  for (int i = m_surv + tid; i < m2; i += kThreads) s_idx[i] = kPad;
+  __syncthreads();
+
+  // ---- 5. bitonic sort of survivors by (e, t, tie) ----
+  auto tie_of = [&](uint32_t i) -> uint64_t {
+    if (a.tie) return a.tie[i];
+    if (a.id) return a.id[p0 + i];
+    return (uint64_t)i;
+  };
+  auto less = [&](uint32_t x, uint32_t y) -> bool {
+    if (x == kPad) return false;
+    if (y == kPad) return true;
+    const double ex = pe[x], ey = pe[y];
+    if (ex != ey) return ex < ey;
+    const double tx = pt[x], ty = pt[y];
+    if (tx != ty) return tx < ty;
+    return tie_of(x) < tie_of(y);
+  };
+  for (int k = 2; k <= m2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < m2; i += kThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint32_t x = s_idx[i], y = s_idx[ixj];
+          const bool asc = (i & k) == 0;
+          if (less(y, x) == asc) { s_idx[i] = y; s_idx[ixj] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- 6. exact filter: keep iff t <= min t over strictly lower e ----
+  const int m = (int)m_surv;
+  for (int p = tid; p < m; p += kThreads) {
+    const uint32_t i = s_idx[p];
+    s_pm[p] = pt[i];
+    s_gs[p] = (p == 0 || pe[i] != pe[s_idx[p - 1]]) ? (uint32_t)p : 0u;
+  }
+  __syncthreads();
+  block_scan_incl(s_pm, m, s_part, MinD(), (double)INFINITY);
+  block_scan_incl(s_gs, m, reinterpret_cast<uint32_t*>(s_part), MaxU(), 0u);
+  // keep flags -> positions (reuse s_gs after reading the group start)
+  for (int p0i = 0; p0i < m; p0i += kThreads) {
+    const int p = p0i + tid;
+    uint32_t keep = 0;
+    if (p < m) {
+      const uint32_t gs = s_gs[p];
+      keep = (gs == 0u) ? 1u : (pt[s_idx[p]] <= s_pm[gs - 1] ? 1u : 0u);
+    }
+    __syncthreads();
+    if (p < m) s_gs[p] = keep;
+  }
+  __syncthreads();
+  // s_pm no longer needed past this point for p beyond gs lookups: all reads done above
+  block_scan_incl(s_gs, m, reinterpret_cast<uint32_t*>(s_part), AddU(), 0u);
+  const uint32_t f = m > 0 ? s_gs[m - 1] : 0u;
+  if (tid == 0) {
+    if (a.front_n) a.front_n[g] = f;
+    if (a.front_idx && (int64_t)f > a.cap_front && a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
+    if (a.out_count) s_base = atomicAdd(a.out_count, (unsigned long long)f);
+  }
+  __syncthreads();
+  const unsigned long long obase = a.out_count ? s_base : 0ull;
+  if (a.out_count && obase + f > (unsigned long long)a.out_cap) {
+    if (tid == 0 && a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
+  }
+  for (int p = tid; p < m; p += kThreads) {
+    const uint32_t incl = s_gs[p];
+    const uint32_t prev = p > 0 ? s_gs[p - 1] : 0u;
+    if (incl != prev) {
+      const uint32_t rank = prev;
+      const uint32_t i = s_idx[p];
+      if (a.front_idx && (int64_t)rank < a.cap_front) a.front_idx[g * a.cap_front + rank] = i;
+      if (a.out_count && obase + rank < (unsigned long long)a.out_cap) {
+        a.out_e[obase + rank] = pe[i];
+        a.out_t[obase + rank] = pt[i];
+        a.out_id[obase + rank] = a.id ? a.id[p0 + i] : (uint64_t)(p0 + i);
+      }
+    }
+  }
+}
+
+struct Plan { int resident; int surv_cap; size_t smem; };
+
+Plan plan_groups(const FfbContext* ctx, int64_t group_size) {
+  Plan p;
+  int64_t mc = 1;
+  while (mc < group_size && mc < 2048) mc <<= 1;
+  if (mc < 32) mc = 32;
+  const size_t fixed = (size_t)mc * (8 + 4 + 4);
+  const size_t limit = ctx->smem_optin ? ctx->smem_optin - 4096 : 96 * 1024;
+  const size_t budget2 = 100 * 1024;   // keeps two CTAs per SM resident
+  size_t res_bytes = (size_t)group_size * 16;
+  p.resident = (fixed + res_bytes <= limit) ? 1 : 0;
+  // grow the survivor capacity when shared memory is spare and the group is large
+  if (p.resident && fixed + res_bytes > budget2) {
+    while (mc < group_size && (size_t)(mc * 2) * 16 + res_bytes <= limit) mc <<= 1;
+  }
+  if (!p.resident) {
+    while (mc < group_size && (size_t)(mc * 2) * 16 <= limit) mc <<= 1;
+  }
+  p.surv_cap = (int)mc;
+  p.smem = (size_t)mc * 16 + (p.resident ? res_bytes : 0);
+  return p;
+}
+
+int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t stream) {
+  Plan p = plan_groups(ctx, a.group_size);
+  a.resident = p.resident;
+  a.surv_cap = p.surv_cap;
+  if (n_groups > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "skyline: too many groups for one launch");
+  FFB_CUDA(ctx, cudaFuncSetAttribute(skyline_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+  FFB_LAUNCH(skyline_group_kernel, (unsigned)n_groups, kThreads, p.smem, stream, a);
+  return ffb_check_launch(ctx, "skyline_group_kernel");
+}
+
+}  // namespace
+
+extern "C" int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const double* d_t,
+                                      int64_t n_groups, int64_t group_size, const uint32_t* d_tie,
+                                      double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
+                                      double* d_tpeak, int64_t cap_front, uint32_t* d_status,
+                                      void* stream) {
+  if (!ctx || !d_e || !d_t || n_groups < 0 || group_size <= 0 || group_size > 0x7fffffffLL || cap_front < 0)
+    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline_groups: bad argument");
+  if (!(rho <= 1.0)) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline_groups: rho must be <= 1");
+  if (n_groups == 0) return FFB_OK;
+  FFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  SkyArgs a = {};
+  a.e = d_e; a.t = d_t; a.id = nullptr; a.tie = d_tie;
+  a.n_total = n_groups * group_size; a.group_size = group_size; a.rho = rho;
+  a.front_idx = d_front_idx; a.front_n = d_front_n; a.tpeak = d_tpeak; a.cap_front = cap_front;
+  a.status = d_status;
+  return launch_groups(ctx, a, n_groups, (cudaStream_t)stream);
+}
+
+extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double* d_t, const double* d_occ,
+                               const uint64_t* d_id, int64_t n, double rho, uint64_t* d_front_id,
+                               double* d_front_e, double* d_front_t, int64_t cap_front,
+                               int64_t* h_front_n, double* h_tpeak, void* stream_) {
+  if (!ctx || !d_e || !d_t || n < 0 || !h_front_n || cap_front <= 0 || !d_front_id)
+    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline: bad argument");
+  if (d_occ) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline: 3-objective fronts are not built yet");
+  if (!(rho <= 1.0)) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline: rho must be <= 1");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  *h_front_n = 0;
+  if (h_tpeak) *h_tpeak = INFINITY;
+  if (n == 0) return FFB_OK;
+  FFB_CUDA(ctx, cudaSetDevice(ctx->device));
+
+  // Level structure: chunk fronts -> compact buffer -> ... -> one group.  The floor is
+  // applied on the last level only: front(floor(X)) == floor(front(X)) because a dominator
+  // has strictly smaller t and is therefore itself eligible.
+  const int64_t chunk = 4096;
+  int64_t work_cap = n / 8 + 4 * chunk;
+  if (work_cap < cap_front) work_cap = cap_front;
+  // scratch: two ping-pong triples + counters/status
+  const size_t tri = (size_t)work_cap * 24;
+  int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 2 * tri + 256);
+  if (rc) return rc;
+  char* base = (char*)ctx->d_sky.p;
+  double* buf_e[2] = {(double*)base, (double*)(base + tri)};
+  double* buf_t[2] = {buf_e[0] + work_cap, buf_e[1] + work_cap};
+  uint64_t* buf_id[2] = {(uint64_t*)(buf_t[0] + work_cap), (uint64_t*)(buf_t[1] + work_cap)};
+  unsigned long long* d_count = (unsigned long long*)(base + 2 * tri);
+  uint32_t* d_status = (uint32_t*)(d_count + 4);
+  double* d_tp = (double*)(d_count + 8);
+
+  const double* cur_e = d_e; const double* cur_t = d_t; const uint64_t* cur_id = d_id;
+  int64_t cur_n = n;
+  int which = 0;
+  FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
+  for (int level = 0; level < 64; ++level) {
+    const bool last = cur_n <= chunk;
+    const int64_t n_groups = (cur_n + chunk - 1) / chunk;
+    SkyArgs a = {};
+    a.e = cur_e; a.t = cur_t; a.id = cur_id; a.tie = nullptr;
+    a.n_total = cur_n; a.group_size = last ? cur_n : chunk;
+    a.rho = last ? rho : 0.0;
+    a.status = d_status;
+    a.out_count = d_count + (level & 3);
+    if (last) {
+      a.out_e = d_front_e ? d_front_e : buf_e[which]; a.out_t = d_front_t ? d_front_t : buf_t[which];
+      a.out_id = d_front_id; a.out_cap = d_front_e && d_front_t ? cap_front : (cap_front < work_cap ? cap_front : work_cap);
+      a.tpeak = d_tp;
+    } else {
+      a.out_e = buf_e[which]; a.out_t = buf_t[which]; a.out_id = buf_id[which]; a.out_cap = work_cap;
+    }
+    FFB_CUDA(ctx, cudaMemsetAsync(a.out_count, 0, sizeof(unsigned long long), stream));
+    rc = launch_groups(ctx, a, last ? 1 : n_groups, stream);
+    if (rc) return rc;
+    unsigned long long h_count = 0; uint32_t h_status = 0;
+    FFB_CUDA(ctx, cudaMemcpyAsync(&h_count, a.out_count, sizeof(h_count), cudaMemcpyDeviceToHost, stream));
+    FFB_CUDA(ctx, cudaMemcpyAsync(&h_status, d_status, sizeof(h_status), cudaMemcpyDeviceToHost, stream));
+    FFB_CUDA(ctx, cudaStreamSynchronize(stream));
+    if (h_status & (1u << FFB_E_CAPACITY))
+      return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: front exceeds capacity at level %d (%llu candidates kept of %lld)",
+                      level, h_count, (long long)cur_n);
+    if (last) {
+      *h_front_n = (int64_t)h_count;
+      if (h_tpeak) {
+        // t_peak of the whole set = min t = min over the final group (the min-t point is
+        // never dominated, so it reaches the last level)
+        FFB_CUDA(ctx, cudaMemcpyAsync(h_tpeak, d_tp, sizeof(double), cudaMemcpyDeviceToHost, stream));
+        FFB_CUDA(ctx, cudaStreamSynchronize(stream));
+      }
+      return FFB_OK;
+    }
+    if ((int64_t)h_count * 2 > cur_n && cur_n > 4 * chunk)
+      return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: candidate set does not reduce (%llu of %lld on chunk fronts)",
+                      h_count, (long long)cur_n);
+    cur_e = buf_e[which]; cur_t = buf_t[which]; cur_id = buf_id[which];
+    cur_n = (int64_t)h_count;
+    which ^= 1;
+  }
+  return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: level limit reached");
+}
