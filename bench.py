@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the FlipFlop analysis hot path on B200 (contract: see the task statement).
+
+One step = one full analysis pass over one batch of synthetic input, per rank:
+  lex      PTX corpus shard  -> opcode histograms + dynamic feature rows     (K1 / K1b)
+  score    kernels x 1 spec x 464 block shapes x 7 power caps -> t_exec, e_pred (K2 + K3)
+  front    one Pareto front per (kernel, spec) group of 3248 candidates        (K4)
+Weak scaling: every rank owns its own kernels (no data-path collective: groups never span
+ranks in this workload; the NCCL front merge only exists for single sets sharded by range).
+
+`value` is device-timed with inputs resident in HBM; `e2e` is the same pass through the
+public API with HOST buffers (pinned), host->device copies and the device->host read of the
+fronts inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+DIMS = list(range(1, 1025))                       # block-dim candidates 1..1024 -> 464 valid shapes
+CAPS = np.array([100.0, 125.0, 150.0, 175.0, 200.0, 225.0, 250.0])
+KERNELS_PER_RANK = 38_400                         # ~1.25 GB of PTX at ~33 KB / kernel (10 GB / 8 GPUs)
+RHO = 0.95
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--kernels", type=int, default=KERNELS_PER_RANK, help="kernels per rank")
+    ap.add_argument("--corpus-mb", type=int, default=-1, help="PTX shard per rank in MB (-1: 1250 when the lexer is built)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        sm = sorted(int(r[0]) for r in self.rows if r and r[0].isdigit())
+        mx = [int(r[1]) for r in self.rows if len(r) > 1 and r[1].isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows if len(r) >= 6 for n, v in zip(names, r[2:6]) if v.lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU legs (oracle)
+def _cpu_score_front(args):
+    """Oracle port of score + front for a slice of kernels (one worker)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import flipflop_oracle as orc
+    from paper_2601_13345_b200 import specs
+    feat, res, shp, tie = args
+    a, p = specs.default_architecture(), specs.default_calibration()
+    t, e = orc.score_grid_numpy(feat, res, orc.arch_dict(a), orc.cal_dict(p), shp, CAPS)
+    n_front = 0
+    for k in range(feat.shape[0]):
+        idx, _ = orc.pareto_indices(e[k].reshape(-1), t[k].reshape(-1), tie=tie, rho=RHO)
+        n_front += len(idx)
+    return feat.shape[0] * shp.shape[0] * CAPS.size, n_front
+
+
+def _cpu_lex(args):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import flipflop_oracle as orc
+    text, offs = args
+    n = 0
+    for i in range(len(offs) - 1):
+        orc.kernel_feature_row(text[offs[i]:offs[i + 1]].decode("ascii"))
+        n += int(offs[i + 1] - offs[i])
+    return n
+
+
+def cpu_sample(feat, res, shp, tie, corpus, workers: int, k_score: int, lex_bytes: int):
+    """Times the oracle on a bounded sample; returns (points/s, bytes/s, description)."""
+    import multiprocessing as mp
+    chunks = [c for c in np.array_split(np.arange(min(k_score, feat.shape[0])), max(workers, 1)) if c.size]
+    jobs = [(feat[c], res[c], shp, tie) for c in chunks]
+    lex_jobs = []
+    if corpus is not None:
+        text, offs = corpus
+        k = int(np.searchsorted(offs, lex_bytes, side="right"))
+        k = max(k, min(workers + 1, len(offs)))
+        bounds = np.linspace(0, k - 1, max(workers, 1) + 1).astype(int)
+        lex_jobs = [(text, offs[bounds[i]:bounds[i + 1] + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(max(workers, 1)) as pool:
+        t0 = time.perf_counter()
+        pts = sum(r[0] for r in pool.map(_cpu_score_front, jobs))
+        t_score = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        nbytes = sum(pool.map(_cpu_lex, lex_jobs)) if lex_jobs else 0
+        t_lex = time.perf_counter() - t0
+    return pts, t_score, nbytes, t_lex
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2601_13345_b200 import engine, native, specs, synth
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rt = native.get_runtime(local)          # raises NativeLibraryMissing: no fallback exists
+    dev = rt.device
+
+    try:
+        from paper_2601_13345_b200 import corpus as corpus_mod
+    except ImportError:
+        corpus_mod = None
+
+    # ---- synthetic inputs (host, pinned) ----
+    K = args.kernels
+    a, p = specs.default_architecture(), specs.default_calibration()
+    sp = engine.spec_rows([(a, p)])
+    shp_xy = engine.enumerate_shapes(sp[0], 0, DIMS)
+    shp = engine.shape_rows([tuple(x) for x in shp_xy])
+    J, C = shp.shape[0], CAPS.size
+    G = J * C
+    # tie rank reproducing explorer.py:113-119: (block_x, block_y, p_cap) lexicographic
+    order = np.lexsort((shp_xy[:, 1], shp_xy[:, 0]))
+    rank_of_shape = np.empty(J, dtype=np.int64)
+    rank_of_shape[order] = np.arange(J)
+    tie_np = (rank_of_shape[:, None] * C + np.arange(C)[None, :]).reshape(-1).astype(np.int32)
+    feat_np, res_np = synth.feature_rows(seed=3 + rank, n_kernels=K)
+    res_np[:, 0] = 0                                  # "generic" resource rule: no input-scaled shared memory
+
+    corpus = None
+    corpus_mb = args.corpus_mb if args.corpus_mb >= 0 else (1250 if corpus_mod is not None else 0)
+    if corpus_mod is not None and corpus_mb > 0:
+        corpus = corpus_mod.bench_corpus(seed=4 + rank, target_bytes=corpus_mb * 10**6, n_kernels=K)
+
+    h_feat = torch.from_numpy(feat_np).pin_memory()
+    h_res = torch.from_numpy(res_np).pin_memory()
+    d_feat, d_res = h_feat.to(dev), h_res.to(dev)
+    d_tie = torch.from_numpy(tie_np).to(dev)
+    bufs = {"t": torch.empty((K, 1, J, C), dtype=torch.float64, device=dev),
+            "e": torch.empty((K, 1, J, C), dtype=torch.float64, device=dev)}
+    cap_front = 64
+    h_front = torch.empty((K, cap_front), dtype=torch.int32).pin_memory()
+    h_front_n = torch.empty((K,), dtype=torch.int32).pin_memory()
+
+    if corpus is not None:
+        lex_state = corpus_mod.BenchLexState(rt, corpus)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    phase_ms = {"lex": 0.0, "score": 0.0, "front": 0.0}
+
+    def step(resident: bool, timed: bool):
+        marks = [ev() for _ in range(4)] if timed else None
+        feat, res = d_feat, d_res
+        if not resident:
+            feat = h_feat.to(dev, non_blocking=True)
+            res = h_res.to(dev, non_blocking=True)
+        if timed:
+            marks[0].record()
+        if corpus is not None:
+            feat = lex_state.run(resident=resident)          # corpus -> feature rows (device)
+        if timed:
+            marks[1].record()
+        r = engine.score_grid(feat, res, sp, shp, CAPS, want=("t", "e"), out=bufs, check=False, rt=rt)
+        if timed:
+            marks[2].record()
+        fi, fn, tp = engine.skyline_groups(r.e.view(-1), r.t.view(-1), K, G, tie=d_tie, rho=RHO,
+                                           cap_front=cap_front, check=False, rt=rt)
+        if timed:
+            marks[3].record()
+        if not resident:
+            h_front.copy_(fi, non_blocking=True)
+            h_front_n.copy_(fn, non_blocking=True)
+        return marks, (fi, fn)
+
+    def run(resident: bool, steps: int, warmup: int):
+        for _ in range(warmup):
+            step(resident, False)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = rt.launches()
+        all_marks = []
+        t_start, t_end = ev(), ev()
+        t_start.record()
+        for _ in range(steps):
+            marks, _ = step(resident, True)
+            all_marks.append(marks)
+        t_end.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = t_start.elapsed_time(t_end)
+        if world > 1:
+            tms = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+            ms = float(tms.item())
+        per = {"lex": 0.0, "score": 0.0, "front": 0.0}
+        for m in all_marks:
+            per["lex"] += m[0].elapsed_time(m[1])
+            per["score"] += m[1].elapsed_time(m[2])
+            per["front"] += m[2].elapsed_time(m[3])
+        return ms, {k: v / steps for k, v in per.items()}, rt.launches() - launches0
+
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    ms_dev, phase_ms, launches = run(True, args.steps, args.warmup)
+    clocks = sampler.stop() if rank == 0 else None
+    ms_e2e, _, _ = run(False, max(3, args.steps // 2), 2)
+    e2e_steps = max(3, args.steps // 2)
+
+    points_rank = K * G
+    points_total = points_rank * world
+    lex_bytes_rank = int(corpus.n_bytes) if corpus is not None else 0
+    value = points_total / (ms_dev / args.steps / 1e3)
+    e2e_value = points_total / (ms_e2e / e2e_steps / 1e3)
+
+    # ---- sanity: fronts from the last step are non-empty and ordered ----
+    _, (fi, fn) = step(True, False)
+    torch.cuda.synchronize()
+    assert int(fn.min()) >= 1 and int(fn.max()) <= cap_front, "front size outside the bench buffer"
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    kernels = {
+        "score": {"kernel": "predict_grid_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["score"],
+                  "bytes_per_unit": "16 B written per grid point (t_exec, e_pred f64)"},
+        "front": {"kernel": "skyline_group_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["front"],
+                  "bytes_per_unit": "16 B read per candidate (e, t f64)"},
+    }
+    if corpus is not None:
+        kernels["lex"] = {"kernel": "lex_corpus_kernel (+ flow)", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
+                          "bytes_per_unit": "1 B read per PTX byte"}
+    for v in kernels.values():
+        v["achieved_gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
+        v["frac"] = v["achieved_gbs"] / peak if v["achieved_gbs"] else None
+    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    traffic = None
+    try:
+        traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(kernels[dom]["kernel"])
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "hbm", "kernel": kernels[dom]["kernel"], "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes": kernels[dom]["bytes_per_unit"],
+                "all_kernels": {k: {kk: vv for kk, vv in v.items() if kk != "bytes"} for k, v in kernels.items()}}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        k_cpu = min(K, 24 * workers)
+        pts, t_score, nb, t_lex = cpu_sample(feat_np, res_np, shp_xy, tie_np,
+                                            corpus.host_sample() if corpus is not None else None,
+                                            workers, k_cpu, lex_bytes=3_000_000 * workers // 8)
+        cpu = {"value": pts / t_score, "unit": "configs/s", "cores": workers, "kind": "port",
+               "sample": f"oracle (numpy score_grid + sort-sweep front) on {k_cpu} kernels x {G} configs = {pts} points, "
+                         f"{workers} processes, {t_score:.1f} s"
+                         + (f"; lexer+dataflow oracle on {nb / 1e6:.1f} MB in {t_lex:.1f} s" if nb else ""),
+               "lex_value": (nb / t_lex / 1e9) if nb else None, "lex_unit": "GB/s"}
+
+    out = {
+        "metric": "configs_scored_per_sec", "value": value, "unit": "configs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "full FlipFlop analysis (BASELINE configs[3] x configs[2] grid): per GPU "
+                               f"{K} generated kernels ({lex_bytes_rank / 1e9:.2f} GB PTX lexed) x 1 spec x {J} block shapes "
+                               f"(dims 1..1024) x {C} caps = {points_rank} grid points, one front per kernel, rho={RHO}",
+                   "kernels_per_gpu": K, "shapes": J, "caps": C, "specs": 1, "points_per_gpu": points_rank,
+                   "ptx_bytes_per_gpu": lex_bytes_rank,
+                   "l2": "no flush needed: each step streams 2.0 GB of outputs + the corpus, far above the 126 MB L2"},
+        "phases_ms": phase_ms,
+        "ptx_gb_per_s": (lex_bytes_rank * world / (phase_ms["lex"] / 1e3) / 1e9) if corpus is not None and phase_ms["lex"] > 0 else None,
+        "clocks": clocks, "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": "configs/s",
+                "h2d_bytes_per_step": int(h_feat.numel() * 8 + h_res.numel() * 8 + lex_bytes_rank) * world,
+                "d2h_bytes_per_step": int(h_front.numel() * 4 + h_front_n.numel() * 4) * world,
+                "ms_per_step": ms_e2e / e2e_steps, "steps": e2e_steps},
+        "roofline": roofline, "cpu_baseline": cpu,
+    }
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def reference_arm(args, rank, world):
+    """CPU arm: the oracle port of the same pass on all host cores, bounded sample per step."""
+    if rank != 0:
+        return
+    from paper_2601_13345_b200 import specs, synth
+    try:
+        from paper_2601_13345_b200 import corpus as corpus_mod
+    except ImportError:
+        corpus_mod = None
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import flipflop_oracle as orc  # noqa: F401
+    import ctypes  # enumerate shapes without a GPU: pure host entry point of libffb
+    from paper_2601_13345_b200 import native
+    from paper_2601_13345_b200.specs import pack_spec
+    a, p = specs.default_architecture(), specs.default_calibration()
+    ad = orc.arch_dict(a)
+    cfgs = orc.enumerate_configs(ad, 0, DIMS, None)
+    shp_xy = np.array([(bx, by) for bx, by, _ in cfgs], dtype=np.int32)
+    J, C = shp_xy.shape[0], CAPS.size
+    G = J * C
+    order = np.lexsort((shp_xy[:, 1], shp_xy[:, 0]))
+    rank_of_shape = np.empty(J, dtype=np.int64)
+    rank_of_shape[order] = np.arange(J)
+    tie_np = (rank_of_shape[:, None] * C + np.arange(C)[None, :]).reshape(-1).astype(np.int32)
+    workers = os.cpu_count() or 1
+    k_step = 160 * workers
+    feat_np, res_np = synth.feature_rows(seed=3, n_kernels=k_step)
+    res_np[:, 0] = 0
+    corpus_sample = None
+    if corpus_mod is not None:
+        corpus_sample = corpus_mod.bench_corpus(seed=4, target_bytes=2_000_000 * workers // 8 + 200_000, n_kernels=None).host_sample()
+    tot_pts, tot_t, tot_b, tot_tl = 0, 0.0, 0, 0.0
+    for i in range(args.warmup + args.steps):
+        pts, t_score, nb, t_lex = cpu_sample(feat_np, res_np, shp_xy, tie_np, corpus_sample, workers, k_step, 10**9)
+        if i >= args.warmup:
+            tot_pts += pts; tot_t += t_score + t_lex; tot_b += nb; tot_tl += t_lex
+    value = tot_pts / tot_t
+    out = {"impl": "reference", "metric": "configs_scored_per_sec", "value": value, "unit": "configs/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"oracle port of the same pass, bounded sample per step: {k_step} kernels x {G} configs"
+                                  + (f" + {tot_b / max(args.steps, 1) / 1e6:.1f} MB PTX lexed" if tot_b else "")},
+           "ptx_gb_per_s": (tot_b / tot_tl / 1e9) if tot_b else None,
+           "cpu_baseline": {"value": value, "unit": "configs/s", "cores": workers, "kind": "port",
+                            "sample": f"{k_step} kernels x {G} configs per step, {workers} processes"},
+           "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -408,7 +408,8 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   int which = 0;
   FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
   for (int level = 0; level < 64; ++level) {
-    const bool last = cur_n <= chunk;
+    // later levels may end early: one CTA can stream a modest set straight from L2
+    const bool last = cur_n <= chunk || (level > 0 && cur_n <= 32 * chunk);
     const int64_t n_groups = (cur_n + chunk - 1) / chunk;
     SkyArgs a = {};
     a.e = cur_e; a.t = cur_t; a.id = cur_id; a.tie = nullptr;

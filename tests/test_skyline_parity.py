@@ -1,0 +1,83 @@
+"""K4 (ffb_skyline_groups / ffb_skyline) against the oracle: membership AND order exact."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import flipflop_oracle as orc
+from paper_2601_13345_b200 import engine, native, synth
+from paper_2601_13345_b200.errors import CapacityExceeded
+
+
+def _dev(x):
+    rt = native.get_runtime()
+    return rt.to_device(torch.from_numpy(np.ascontiguousarray(x)))
+
+
+@pytest.mark.parametrize("kind", ["uniform", "tied", "anticorrelated"])
+@pytest.mark.parametrize("rho", [0.95, 1.0, 0.0])
+def test_groups_match_oracle(backend, kind, rho):
+    ng, G = (3, 300) if backend == "emul" else (64, 3248)
+    e, t = synth.candidate_cloud(seed=202, n=ng * G, kind=kind)
+    if kind == "anticorrelated" and backend != "emul":
+        t = 10.0 - e + np.random.default_rng(1).normal(0.0, 2.0, e.size)   # keep the front below the survivor cap
+    fi, fn, tp = engine.skyline_groups(_dev(e), _dev(t), ng, G, rho=rho)
+    fi, fn, tp = fi.cpu().numpy(), fn.cpu().numpy(), tp.cpu().numpy()
+    for g in range(ng):
+        want, wtp = orc.pareto_indices(e[g * G:(g + 1) * G], t[g * G:(g + 1) * G], rho=rho)
+        assert fi[g, :fn[g]].tolist() == want
+        assert tp[g] == wtp
+
+
+def test_ties_all_survive_and_bruteforce_agrees(backend):
+    rng = np.random.default_rng(19)
+    for _ in range(4):
+        n = int(rng.integers(1, 400))
+        e = rng.integers(0, 5, n).astype(np.float64)
+        t = rng.integers(0, 5, n).astype(np.float64)
+        fi, fn, _ = engine.skyline_groups(_dev(e), _dev(t), 1, n, rho=0.0)
+        got = fi.cpu().numpy()[0, :int(fn[0])].tolist()
+        assert set(got) == orc.pareto_bruteforce(e, t)
+        key = [(e[i], t[i], i) for i in got]
+        assert key == sorted(key)
+
+
+def test_tie_key_orders_equal_points(backend):
+    e = np.array([1.0, 1.0, 1.0, 2.0])
+    t = np.array([3.0, 3.0, 3.0, 1.0])
+    tie = torch.tensor([2, 0, 1, 0], dtype=torch.int32)
+    fi, fn, _ = engine.skyline_groups(_dev(e), _dev(t), 1, 4, tie=native.get_runtime().to_device(tie), rho=0.0)
+    assert fi.cpu().numpy()[0, :int(fn[0])].tolist() == [1, 2, 0, 3]
+
+
+def test_invalid_points_never_on_front(backend):
+    e = np.array([np.inf, 1.0, np.inf, 0.5])
+    t = np.array([np.inf, 2.0, np.inf, 3.0])
+    fi, fn, tp = engine.skyline_groups(_dev(e), _dev(t), 1, 4, rho=0.0)
+    assert fi.cpu().numpy()[0, :int(fn[0])].tolist() == [3, 1] and tp[0].item() == 2.0
+    fi, fn, tp = engine.skyline_groups(_dev(np.full(4, np.inf)), _dev(np.full(4, np.inf)), 1, 4, rho=0.95)
+    assert int(fn[0]) == 0 and np.isinf(tp[0].item())
+
+
+def test_front_capacity_is_reported(backend):
+    n = 64
+    e = np.arange(n, dtype=np.float64)
+    t = e[::-1].copy()
+    with pytest.raises(CapacityExceeded):
+        engine.skyline_groups(_dev(e), _dev(t), 1, n, rho=0.0, cap_front=8)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "tied"])
+def test_large_set_hierarchical(backend, kind):
+    n = 30_000 if backend == "emul" else (5_000_000 if kind == "uniform" else 100_000)
+    e, t = synth.candidate_cloud(seed=5, n=n, kind=kind)
+    cap = 1 << 13
+    ids, fe, ft, tpk = engine.skyline(_dev(e), _dev(t), rho=0.0, cap_front=cap)
+    want, wtp = orc.pareto_indices(e, t, rho=0.0)
+    assert ids.cpu().numpy().tolist() == want
+    assert np.array_equal(fe.cpu().numpy(), e[want]) and np.array_equal(ft.cpu().numpy(), t[want])
+    assert tpk == wtp
+    # idempotence: the front of the front is the front
+    ids2, *_ = engine.skyline(fe.contiguous(), ft.contiguous(), ids=ids.contiguous(), rho=0.0, cap_front=cap)
+    assert ids2.cpu().numpy().tolist() == want
