@@ -162,6 +162,64 @@ int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double* d_t, const
                     double* d_front_e, double* d_front_t, int64_t cap_front,
                     int64_t* h_front_n, double* h_tpeak, void* stream);
 
+/* ---- K1: byte-lexer, opcode classifier, per-kernel histogram ---------------------------
+ * Stands in for ptx.py:139-141 (_strip_comments), :165-187 (_find_kernel), :207-293
+ * (parse_ptx statement loop, declarations), :296-313 (_parse_instruction), :99-136
+ * (classify_opcode) and :64-76 (access_bytes), applied to every segment of a corpus:
+ * segment k is text[seg_off[k] : seg_off[k+1]) and is analysed exactly like one
+ * parse_ptx(source) call (first .entry of the segment, or the one named h_kernel_name).
+ *
+ * Documented device capacities (status FFB_E_CAPACITY, never a silent difference):
+ * a physical line, or a multi-line statement, must fit one 4 KB tile; input is ASCII.
+ */
+typedef struct {
+  uint32_t status;          /* FFB_OK or FFB_E_*  (reference exception of parse_ptx)            */
+  uint32_t n_instr;         /* len(PtxModule.instructions)                                      */
+  uint32_t n_labels;        /* label definitions met (duplicates counted)                        */
+  uint32_t n_decls;         /* .reg declarations met                                             */
+  uint64_t static_shared;   /* PtxModule.static_shared_bytes (ptx.py:249-254)                     */
+  uint64_t regs_declared;   /* sum(PtxModule.registers_declared.values()) (features.py:126)       */
+  uint32_t name_off, name_len;   /* kernel name, bytes from the segment start                    */
+  uint32_t body_off, body_end;   /* first byte after '{' and offset of the matching '}'          */
+} FfbSegInfo;
+
+/* 64-byte instruction record and 16-byte label record: see csrc/ffb_records.cuh for the bit
+ * layout of `meta` and of operand descriptors.  Opaque to most callers. */
+typedef struct { uint32_t meta, line, off, len; uint64_t pred, aux, op[4]; } FfbInsRecC;
+typedef struct { uint64_t hash; uint32_t index, off; } FfbLabelRecC;
+
+/* Optional per-instruction text spans so a host can rebuild Instruction strings
+ * (ptx.py:45-54) by slicing the source; offsets are bytes from the segment start. */
+#define FFB_MAX_SPAN_OPS 12
+typedef struct {
+  uint32_t pred_off, pred_len, opc_off, opc_len, n_ops, reserved[3];
+  uint32_t op_off[FFB_MAX_SPAN_OPS], op_len[FFB_MAX_SPAN_OPS];
+} FfbSpanRec;
+
+/* Optional `.reg` declaration records (ptx.py:244-248), FFB_MAX_DECLS per segment. */
+#define FFB_MAX_DECLS 32
+typedef struct { uint32_t cls_off, cls_len; uint64_t count; } FfbDeclRec;
+
+typedef struct {
+  const uint8_t* d_text;      /* corpus bytes; the allocation must be readable up to n_bytes   */
+  int64_t n_bytes;            /* size rounded UP to a multiple of 16                            */
+  const int64_t* d_seg_off;   /* [K+1] segment boundaries (byte offsets, ascending)             */
+  int64_t n_segs;
+  const int32_t* d_order;     /* optional [K]: processing order (e.g. longest first)            */
+  const uint8_t* h_kernel_name; int32_t kernel_name_len;   /* optional parse_ptx(kernel_name=)  */
+  uint32_t* d_hist;           /* [K, FFB_N_CLASSES] static class histogram                      */
+  FfbSegInfo* d_info;         /* [K]                                                            */
+  /* record mode: all NULL, or ins/labels + bases given (bases = exclusive scans of the
+   * n_instr / n_labels a previous histogram-only call returned)                              */
+  const int64_t* d_ins_base;  /* [K] */
+  const int64_t* d_lab_base;  /* [K] */
+  void* d_ins;                /* FfbInsRecC[sum n_instr]                                        */
+  void* d_labels;             /* FfbLabelRecC[sum n_labels]                                     */
+  FfbSpanRec* d_spans;        /* optional, parallel to d_ins                                    */
+  FfbDeclRec* d_decls;        /* optional, [K, FFB_MAX_DECLS]                                   */
+} FfbLexDesc;
+int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
