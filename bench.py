@@ -366,7 +366,7 @@ def reference_arm(args, rank, world):
     res_np[:, 0] = 0
     corpus_sample = None
     if corpus_mod is not None:
-        corpus_sample = corpus_mod.bench_corpus(seed=4, target_bytes=2_000_000 * workers // 8 + 200_000, n_kernels=None).host_sample()
+        corpus_sample = synth.ptx_corpus(4, max(workers, int(workers * 2_500_000 / 40_000)))
     tot_pts, tot_t, tot_b, tot_tl = 0, 0.0, 0, 0.0
     for i in range(args.warmup + args.steps):
         pts, t_score, nb, t_lex = cpu_sample(feat_np, res_np, shp_xy, tie_np, corpus_sample, workers, k_step, 10**9)

@@ -220,6 +220,56 @@ typedef struct {
 } FfbLexDesc;
 int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream);
 
+/* ---- K1b: control flow, trip counts, affine alignment, dynamic counts ------------------
+ * Stands in for ptx.py:277-284 (branch targets), cfg.py:57-279 (build_cfg,
+ * estimate_trip_counts), alignment.py:61-147 (trace_affine_scales,
+ * analyze_memory_alignment) and features.py:62-81 (dynamic_instruction_counts), for every
+ * segment of a corpus, from the records ffb_lex_corpus wrote.  Output: one FFB_F_* row per
+ * segment (override columns cleared, FFB_F_OVR_TEXEC = NaN) ready for ffb_predict_grid.
+ *
+ * Capacities (status FFB_E_CAPACITY): integer literals and affine scales beyond 2^60,
+ * producers with more than five operands whose late operands are registers.
+ */
+typedef struct { uint32_t n_blocks, n_edges, n_loops, reserved; } FfbFlowInfo;
+typedef struct {
+  uint32_t header;        /* block index of the loop header                                   */
+  uint32_t n_body;        /* blocks in the body                                               */
+  double   trip;          /* cfg.py:174-181                                                   */
+  uint64_t label_hash;    /* header label (0 when the header carries none)                    */
+  uint32_t label_off;     /* its name, bytes from the segment start                           */
+  uint32_t has_label;
+} FfbLoopRec;
+
+typedef struct {
+  int64_t n_segs;
+  const FfbSegInfo* d_info;       /* [K] from ffb_lex_corpus                                   */
+  const int64_t* d_ins_base;      /* [K] */
+  const int64_t* d_lab_base;      /* [K] */
+  const void* d_ins;              /* FfbInsRecC[n_ins_total]                                   */
+  const void* d_labels;           /* FfbLabelRecC[n_lab_total]                                 */
+  int64_t n_ins_total, n_lab_total;
+  const int32_t* d_order;         /* optional [K] processing order                             */
+  double default_trip;            /* cfg.py:157 (reference default 32.0)                       */
+  const uint64_t* h_ann_hash;     /* optional trip annotations: ffb_name_hash(label) ...       */
+  const double* h_ann_trip;       /* ... -> trip (cfg.py:165-176); applied to every segment    */
+  int32_t n_ann;
+  uint8_t* d_ann_hit;             /* optional [n_ann]: set to 1 when some loop header matched  */
+  double* d_feat;                 /* [K, FFB_FEAT_WIDTH]                                       */
+  uint32_t* d_status;             /* [K] final status (lexer status, or an error found here)   */
+  FfbFlowInfo* d_flow;            /* optional [K]                                              */
+  /* detail outputs for callers that rebuild ControlFlowGraph objects (cfg.py:25-35); all
+   * optional.  Segment k uses slots starting at  o = d_ins_base[k] + 2*k.                     */
+  uint32_t* d_block_start;        /* [n_ins_total + 2K + 8]  n_blocks+1 entries per segment     */
+  int32_t* d_edges;               /* [2*(n_ins_total + 2K + 8), 2]  pairs start at 2*o          */
+  FfbLoopRec* d_loops;            /* [n_ins_total + 2K + 8]                                     */
+  uint8_t* d_loop_body;           /* single-segment use: n_loops x n_blocks membership matrix   */
+  int64_t loop_body_cap;          /* bytes available behind d_loop_body                         */
+  double* d_weights;              /* [n_ins_total + 2K + 8] block weights (cfg.py:43-54)        */
+} FfbFlowDesc;
+int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, void* stream);
+/* 61-bit name hash the lexer assigns to labels / registers (for annotation keys). */
+uint64_t ffb_name_hash(const uint8_t* name, int64_t len);
+
 #ifdef __cplusplus
 }
 #endif

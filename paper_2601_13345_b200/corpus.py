@@ -144,3 +144,164 @@ def lex_records(corp: Corpus, *, kernel_name: str | None = None, spans: bool = F
 
 def raise_segment_status(status: int, what: str = "PTX segment") -> None:
     raise_for_status(int(status), what)
+
+
+# ------------------------------------------------------------------------------ K1b
+FLOW_DTYPE = np.dtype([("n_blocks", "<u4"), ("n_edges", "<u4"), ("n_loops", "<u4"), ("reserved", "<u4")])
+LOOP_DTYPE = np.dtype([("header", "<u4"), ("n_body", "<u4"), ("trip", "<f8"), ("label_hash", "<u8"),
+                       ("label_off", "<u4"), ("has_label", "<u4")])
+assert LOOP_DTYPE.itemsize == 32
+
+
+class FlowDesc(C.Structure):
+    _fields_ = [
+        ("n_segs", C.c_int64), ("d_info", C.c_void_p), ("d_ins_base", C.c_void_p), ("d_lab_base", C.c_void_p),
+        ("d_ins", C.c_void_p), ("d_labels", C.c_void_p), ("n_ins_total", C.c_int64), ("n_lab_total", C.c_int64),
+        ("d_order", C.c_void_p), ("default_trip", C.c_double), ("h_ann_hash", C.c_void_p),
+        ("h_ann_trip", C.c_void_p), ("n_ann", C.c_int32), ("d_ann_hit", C.c_void_p), ("d_feat", C.c_void_p),
+        ("d_status", C.c_void_p), ("d_flow", C.c_void_p), ("d_block_start", C.c_void_p), ("d_edges", C.c_void_p),
+        ("d_loops", C.c_void_p), ("d_loop_body", C.c_void_p), ("loop_body_cap", C.c_int64), ("d_weights", C.c_void_p),
+    ]
+
+
+def name_hash(name: str, rt: native.Runtime | None = None) -> int:
+    rt = rt or native.get_runtime()
+    b = name.encode()
+    return int(rt.lib.ffb_name_hash(b, len(b)))
+
+
+@dataclass
+class FlowResult:
+    feat: torch.Tensor            # float64 [K, FEAT_WIDTH]
+    status: torch.Tensor          # int32 [K]
+    flow: torch.Tensor | None = None         # uint8 [K, 16] (FLOW_DTYPE)
+    block_start: torch.Tensor | None = None
+    edges: torch.Tensor | None = None
+    loops: torch.Tensor | None = None
+    loop_body: torch.Tensor | None = None
+    weights: torch.Tensor | None = None
+    ann_hit: torch.Tensor | None = None
+
+
+def kernel_features(corp: Corpus, lex: LexResult, *, default_trip: float = 32.0, annotations: dict | None = None,
+                    detail: bool = False, out_feat: torch.Tensor | None = None,
+                    rt: native.Runtime | None = None) -> FlowResult:
+    """K1b over the records of ``lex_records``.  No sync."""
+    rt = rt or native.get_runtime()
+    K = corp.n_segs
+    assert lex.ins is not None, "kernel_features needs lex_records() output"
+    feat = out_feat if out_feat is not None else rt.empty((K, native.FEAT_WIDTH), torch.float64)
+    status = rt.empty((K,), torch.int32)
+    res = FlowResult(feat=feat, status=status)
+    n_slots = lex.n_ins + 2 * K + 8
+    ann_hash = ann_trip = None
+    n_ann = 0
+    if annotations:
+        keys = list(annotations)
+        ann_hash = np.asarray([name_hash(k, rt) for k in keys], dtype=np.uint64)
+        ann_trip = np.asarray([float(annotations[k]) for k in keys], dtype=np.float64)
+        n_ann = len(keys)
+        res.ann_hit = torch.zeros(n_ann, dtype=torch.uint8, device=rt.device)
+    if detail:
+        res.flow = torch.zeros((K, 16), dtype=torch.uint8, device=rt.device)
+        res.block_start = torch.zeros(n_slots, dtype=torch.int32, device=rt.device)
+        res.edges = torch.zeros((2 * n_slots, 2), dtype=torch.int32, device=rt.device)
+        res.loops = torch.zeros((n_slots, 32), dtype=torch.uint8, device=rt.device)
+        res.weights = torch.zeros(n_slots, dtype=torch.float64, device=rt.device)
+        if K == 1:
+            res.loop_body = torch.zeros(max(1, min((lex.n_ins + 1) ** 2, 1 << 26)), dtype=torch.uint8, device=rt.device)
+    d = FlowDesc(
+        n_segs=K, d_info=native.ptr(lex.info), d_ins_base=native.ptr(lex.ins_base), d_lab_base=native.ptr(lex.lab_base),
+        d_ins=native.ptr(lex.ins), d_labels=native.ptr(lex.labels), n_ins_total=lex.n_ins, n_lab_total=lex.n_lab,
+        d_order=native.ptr(corp.order), default_trip=float(default_trip),
+        h_ann_hash=ann_hash.ctypes.data if n_ann else None, h_ann_trip=ann_trip.ctypes.data if n_ann else None,
+        n_ann=n_ann, d_ann_hit=native.ptr(res.ann_hit), d_feat=native.ptr(feat), d_status=native.ptr(status),
+        d_flow=native.ptr(res.flow), d_block_start=native.ptr(res.block_start), d_edges=native.ptr(res.edges),
+        d_loops=native.ptr(res.loops), d_loop_body=native.ptr(res.loop_body),
+        loop_body_cap=int(res.loop_body.numel()) if res.loop_body is not None else 0, d_weights=native.ptr(res.weights))
+    rc = rt.lib.ffb_kernel_features(rt.ctx, C.byref(d), rt.stream())
+    rt.check(rc, "ffb_kernel_features")
+    return res
+
+
+def analyze_corpus(corp: Corpus, *, default_trip: float = 32.0, rt: native.Runtime | None = None):
+    """text -> (LexResult, FlowResult): class histograms + one feature row per kernel."""
+    lex = lex_records(corp, rt=rt)
+    return lex, kernel_features(corp, lex, default_trip=default_trip, rt=rt)
+
+
+# ------------------------------------------------------------------------------ bench / smoke helpers
+def bench_corpus(seed: int, target_bytes: int, n_kernels: int | None, *, base_kernels: int = 1200,
+                 rt: native.Runtime | None = None) -> Corpus:
+    """Synthetic corpus of about ``target_bytes``: ``base_kernels`` generated kernels (seeded
+    grammar, synth.ptx_corpus) tiled on the device.  With ``n_kernels`` given the kernel count is
+    exact and the byte size follows (each kernel is ~40 KB on average)."""
+    from . import synth
+    if n_kernels is not None:
+        base_kernels = min(base_kernels, n_kernels)
+        reps = max(1, n_kernels // base_kernels)
+        base_kernels = n_kernels // reps
+    text, offs = synth.ptx_corpus(seed, base_kernels)
+    if n_kernels is None:
+        reps = max(1, int(round(target_bytes / max(len(text), 1))))
+        if reps == 1 and len(text) > 2 * target_bytes:          # small CPU samples: cut at a kernel boundary
+            k = max(1, int(np.searchsorted(offs, target_bytes, side="right")) - 1)
+            text, offs = text[: int(offs[k])], offs[: k + 1]
+    rt = rt or native.get_runtime()
+    n = len(text)
+    dev_base = rt.to_device(torch.frombuffer(bytearray(text), dtype=torch.uint8))
+    total = n * reps
+    padded = (total + 15) // 16 * 16 + 16
+    dev = torch.full((padded,), 10, dtype=torch.uint8, device=rt.device)
+    dev[:total].view(reps, n).copy_(dev_base.unsqueeze(0).expand(reps, n))
+    seg = (offs[None, :-1] + (np.arange(reps, dtype=np.int64) * n)[:, None]).reshape(-1)
+    seg = np.concatenate([seg, [total]]).astype(np.int64)
+    order = rt.to_device(torch.from_numpy(np.argsort(-np.diff(seg), kind="stable").astype(np.int32)))
+    return Corpus(text=dev, n_bytes=total, seg_off=rt.to_device(torch.from_numpy(seg)), n_segs=len(seg) - 1,
+                  order=order, host_text=text, host_off=offs)
+
+
+class BenchLexState:
+    """Preallocated buffers so the timed loop launches kernels only (no allocation, one sync-free
+    pass: record buffers are sized once from a warm-up histogram pass)."""
+
+    def __init__(self, rt: native.Runtime, corp: Corpus):
+        self.rt, self.corp = rt, corp
+        self.lex = lex_records(corp, rt=rt)                  # sizes the record buffers (syncs, untimed)
+        self.feat = rt.empty((corp.n_segs, native.FEAT_WIDTH), torch.float64)
+        self.host_text = None
+
+    def pin_host(self):
+        if self.host_text is None:
+            self.host_text = torch.empty(self.corp.padded_bytes, dtype=torch.uint8).pin_memory()
+            self.host_text.copy_(self.corp.text)
+        return self.host_text
+
+    def run(self, resident: bool = True) -> torch.Tensor:
+        rt, corp, lex = self.rt, self.corp, self.lex
+        if not resident:
+            corp.text.copy_(self.pin_host(), non_blocking=True)           # H2D inside the timed region
+        _call_lex(rt, corp, lex.hist, lex.info)                           # K1 histogram + counts
+        counts = lex.info_i32()[:, 1:3].to(torch.int64)
+        base = (torch.cumsum(counts, dim=0) - counts)
+        lex.ins_base.copy_(base[:, 0]); lex.lab_base.copy_(base[:, 1])
+        _call_lex(rt, corp, lex.hist, lex.info, ins_base=lex.ins_base, lab_base=lex.lab_base, ins=lex.ins,
+                  labels=lex.labels)                                      # K1 records
+        kernel_features(corp, lex, out_feat=self.feat, rt=rt)             # K1b
+        return self.feat
+
+
+def smoke_check(rt: native.Runtime) -> None:
+    """One small corpus through K1 + K1b on the GPU, compared with the oracle."""
+    import flipflop_oracle as orc           # test infrastructure, only reachable from smoke()
+    from . import synth
+    text, offs = synth.ptx_corpus(seed=2, n_kernels=24, lo=30, hi=400)
+    corp = upload_corpus(text, offs, rt=rt)
+    lex, fl = analyze_corpus(corp, rt=rt)
+    hist, feat, status = lex.hist.cpu().numpy(), fl.feat.cpu().numpy(), fl.status.cpu().numpy()
+    for k in range(corp.n_segs):
+        src = text[offs[k]:offs[k + 1]].decode("ascii")
+        kern = orc.parse_kernel(src)
+        assert status[k] == 0 and hist[k].tolist() == orc.class_histogram(kern), f"histogram differs (kernel {k})"
+        want = np.asarray(orc.kernel_feature_row(src), dtype=np.float64)
+        assert feat[k, :11].tobytes() == want.tobytes(), f"feature row differs (kernel {k})"

@@ -1,0 +1,607 @@
+// K1b: per-kernel control-flow and affine dataflow over the lexer's instruction records
+// -> trip-weighted dynamic counts and aligned_fraction (one FFB_F_* feature row per kernel).
+//
+// Restates pkg/src/ptxwatt: ptx.py:277-284 (branch targets must be labels), cfg.py:57-95
+// (leaders, blocks, edges), :98-151 (dominators, natural loops, one loop per header),
+// :154-182 (trip precedence: annotation > detected > default, floored at 1), :191-279
+// (counted do-while recogniser), :43-54 (block weights), alignment.py:31-125 (register ->
+// %tid.x scale map, single textual pass) and :128-147 (weighted aligned fraction),
+// features.py:62-81 (dynamic counts).
+//
+// One THREAD per kernel: the analysis is a chain of sequential, data-dependent walks over a
+// few hundred to a few thousand 64-byte records, so the parallelism is across the tens of
+// thousands of kernels of a corpus (threads of a warp take neighbouring entries of the
+// longest-first order, i.e. kernels of similar length).  All working arrays live in a
+// context-owned HBM scratch indexed by the same exclusive scans as the records.
+//
+// Dominators: the reference iterates full bit-sets to the maximal fixed point.  For blocks
+// reachable from block 0 that equals the dominator tree (computed here with the
+// Cooper-Harvey-Kennedy iteration over a reverse post-order); blocks NOT reachable keep the
+// full set, i.e. every block "dominates" them — reproduced explicitly (dominates()).
+#include "ffb_records.cuh"
+
+#include <math.h>
+
+namespace {
+
+constexpr int kFlowThreads = 64;
+constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
+constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
+constexpr uint32_t kNoBlock = 0xffffffffu;
+
+struct FlowArgs {
+  int64_t n_segs;
+  const FfbSegInfo* info;
+  const int64_t* ins_base;
+  const int64_t* lab_base;
+  const FfbInsRec* ins;
+  const FfbLabelRec* labels;
+  const int32_t* order;
+  double default_trip;
+  const uint64_t* ann_hash;     // device copies
+  const double* ann_trip;
+  int n_ann;
+  uint8_t* ann_hit;             // [n_ann] set when a loop header carries the label
+  double* feat;
+  uint32_t* status;
+  FfbFlowInfo* flow;
+  // scratch (see host side for the carve-up)
+  uint32_t* block_of;           // [N]
+  uint32_t* block_start;        // [N + 2K]
+  int32_t* succ0;               // [N + 2K]
+  int32_t* succ1;
+  uint32_t* pred_ptr;           // [N + 2K]
+  uint32_t* pred_list;          // [2(N + 2K)]
+  int32_t* rpo_num;             // [N + 2K]
+  uint32_t* rpo_order;
+  int32_t* idom;
+  uint32_t* mark;
+  uint32_t* stack;
+  double* weight;               // [N + 2K]
+  uint64_t* lab_key;            // [2L + 4K]
+  uint32_t* lab_first;
+  uint32_t* lab_last;
+  uint64_t* sc_key;             // [2N + 4K]
+  int64_t* sc_val;
+  // detail outputs (optional)
+  uint32_t* out_block_start;
+  int32_t* out_edges;
+  FfbLoopRec* out_loops;
+  uint8_t* out_loop_body;
+  int64_t loop_body_cap;
+  double* out_weights;
+};
+
+// ---- tiny open-addressing tables ----------------------------------------------------------------
+FFB_D uint32_t slot_of(uint64_t h, uint32_t cap) { return (uint32_t)((h * 0x9E3779B97F4A7C15ull) >> 33) % cap; }
+
+struct LabelTable {
+  uint64_t* key; uint32_t* first; uint32_t* last; uint32_t cap;
+  FFB_D void clear() { for (uint32_t i = 0; i < cap; ++i) key[i] = 0; }
+  FFB_D uint32_t find(uint64_t h) const {          // slot or cap
+    uint32_t s = slot_of(h, cap);
+    for (uint32_t n = 0; n < cap; ++n) {
+      if (key[s] == 0) return cap;
+      if (key[s] == h + 1) return s;
+      s = s + 1 == cap ? 0 : s + 1;
+    }
+    return cap;
+  }
+  FFB_D void define(uint64_t h, uint32_t order, uint32_t /*unused*/) {
+    uint32_t s = slot_of(h, cap);
+    for (;;) {
+      if (key[s] == 0) { key[s] = h + 1; first[s] = order; last[s] = order; return; }
+      if (key[s] == h + 1) { last[s] = order; return; }
+      s = s + 1 == cap ? 0 : s + 1;
+    }
+  }
+};
+
+struct ScaleTable {
+  uint64_t* key; int64_t* val; uint32_t cap;
+  FFB_D void clear() { for (uint32_t i = 0; i < cap; ++i) key[i] = 0; }
+  FFB_D int64_t get(uint64_t h) const {
+    uint32_t s = slot_of(h, cap);
+    for (uint32_t n = 0; n < cap; ++n) {
+      if (key[s] == 0) return kNoneScale;
+      if (key[s] == h + 1) return val[s];
+      s = s + 1 == cap ? 0 : s + 1;
+    }
+    return kNoneScale;
+  }
+  FFB_D void put(uint64_t h, int64_t v) {
+    uint32_t s = slot_of(h, cap);
+    for (;;) {
+      if (key[s] == 0 || key[s] == h + 1) { key[s] = h + 1; val[s] = v; return; }
+      s = s + 1 == cap ? 0 : s + 1;
+    }
+  }
+};
+
+// ---- scale arithmetic with saturation -------------------------------------------------------------
+FFB_D bool sc_known(int64_t v) { return v != kNoneScale; }
+FFB_D int64_t sc_add(int64_t a, int64_t b) {
+  if (!sc_known(a) || !sc_known(b)) return kNoneScale;
+  if (a == kBigScale || b == kBigScale) return kBigScale;
+  const int64_t lim = (int64_t)1 << 61;
+  const int64_t r = a + b;     // |a|,|b| <= 2^61: no wrap
+  return (r > lim || r < -lim) ? kBigScale : r;
+}
+FFB_D int64_t sc_neg(int64_t a) { return (!sc_known(a) || a == kBigScale) ? a : -a; }
+FFB_D int64_t sc_mul(int64_t a, int64_t b) {
+  if (!sc_known(a) || !sc_known(b)) return kNoneScale;
+  if (a == 0 || b == 0) return 0;
+  if (a == kBigScale || b == kBigScale) return kBigScale;
+  const int64_t lim = (int64_t)1 << 61;
+  const uint64_t ua = a < 0 ? (uint64_t)(-a) : (uint64_t)a, ub = b < 0 ? (uint64_t)(-b) : (uint64_t)b;
+  if (__umul64hi(ua, ub) != 0) return kBigScale;
+  const uint64_t p = ua * ub;
+  if (p > (uint64_t)lim) return kBigScale;
+  return ((a < 0) != (b < 0)) ? -(int64_t)p : (int64_t)p;
+}
+
+// alignment.py:31-47 on a descriptor
+FFB_D int64_t operand_scale(uint64_t d, const ScaleTable& t) {
+  switch (ffb_op_kind(d)) {
+    case FFB_OPK_TIDX: return 1;
+    case FFB_OPK_UNKNOWN: return kNoneScale;
+    case FFB_OPK_REG: return t.get(ffb_op_hash(d));
+    case FFB_OPK_NONE: return kNoneScale;
+    default: return 0;       // UNIFORM, UNIFORM_REG, INT, BIGINT
+  }
+}
+FFB_D bool is_int_lit(uint64_t d) { const uint64_t k = ffb_op_kind(d); return k == FFB_OPK_INT || k == FFB_OPK_BIGINT; }
+FFB_D int64_t int_as_scale(uint64_t d) { return ffb_op_kind(d) == FFB_OPK_INT ? ffb_op_int(d) : kBigScale; }
+FFB_D bool starts_with_percent(uint64_t d) {
+  const uint64_t k = ffb_op_kind(d);
+  return k == FFB_OPK_REG || k == FFB_OPK_TIDX || k == FFB_OPK_UNKNOWN || k == FFB_OPK_UNIFORM_REG;
+}
+
+// alignment.py:50-58 (_combine_mul)
+FFB_D int64_t mul_scale(uint64_t a, uint64_t b, const ScaleTable& t) {
+  const int64_t sa = operand_scale(a, t), sb = operand_scale(b, t);
+  if (sa == 0 && sb == 0) return 0;
+  if (is_int_lit(b) && sc_known(sa)) return sc_mul(sa, int_as_scale(b));
+  if (is_int_lit(a) && sc_known(sb)) return sc_mul(int_as_scale(a), sb);
+  return kNoneScale;
+}
+
+// dom(h, u): h in the reference's dominator set of u
+FFB_D bool dominates(const int32_t* idom, const int32_t* rpo_num, uint32_t h, uint32_t u) {
+  if (rpo_num[u] < 0) return true;          // unreachable blocks keep the full set (cfg.py:108-122)
+  if (rpo_num[h] < 0) return h == u;
+  uint32_t x = u;
+  for (;;) {
+    if (x == h) return true;
+    if (x == 0) return false;
+    x = (uint32_t)idom[x];
+  }
+}
+
+__global__ void __launch_bounds__(kFlowThreads)
+flow_kernel(FlowArgs a) {
+  const int64_t w = (int64_t)blockIdx.x * kFlowThreads + threadIdx.x;
+  if (w >= a.n_segs) return;
+  const int64_t k = a.order ? (int64_t)a.order[w] : w;
+  const FfbSegInfo inf = a.info[k];
+  double* feat = a.feat + k * FFB_FEAT_WIDTH;
+  for (int c = 0; c < FFB_FEAT_WIDTH; ++c) feat[c] = 0.0;
+  feat[FFB_F_OVR_TEXEC] = NAN;
+  uint32_t status = inf.status;
+  FfbFlowInfo fi;
+  fi.n_blocks = fi.n_edges = fi.n_loops = 0; fi.reserved = 0;
+  if (status != FFB_OK) { a.status[k] = status; if (a.flow) a.flow[k] = fi; return; }
+
+  const uint32_t n = inf.n_instr, L = inf.n_labels;
+  const int64_t ib = a.ins_base[k], lb = a.lab_base[k];
+  const FfbInsRec* ins = a.ins + ib;
+  const FfbLabelRec* lab = a.labels + lb;
+  const int64_t o1 = ib + 2 * k;                   // offset into the [N + 2K] arrays
+  uint32_t* block_of = a.block_of + ib;
+  uint32_t* block_start = a.block_start + o1;
+  int32_t* succ0 = a.succ0 + o1;
+  int32_t* succ1 = a.succ1 + o1;
+  uint32_t* pred_ptr = a.pred_ptr + o1;
+  uint32_t* pred_list = a.pred_list + 2 * o1;
+  int32_t* rpo_num = a.rpo_num + o1;
+  uint32_t* rpo_order = a.rpo_order + o1;
+  int32_t* idom = a.idom + o1;
+  uint32_t* mark = a.mark + o1;
+  uint32_t* stack = a.stack + o1;
+  double* weight = a.weight + o1;
+  LabelTable lt;
+  lt.key = a.lab_key + 2 * lb + 4 * k; lt.first = a.lab_first + 2 * lb + 4 * k; lt.last = a.lab_last + 2 * lb + 4 * k;
+  lt.cap = 2 * L + 3;
+  ScaleTable st;
+  st.key = a.sc_key + 2 * ib + 4 * k; st.val = a.sc_val + 2 * ib + 4 * k; st.cap = 2 * n + 3;
+
+  // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
+  lt.clear();
+  for (uint32_t i = 0; i < L; ++i) lt.define(lab[i].hash, i, 0);
+  // ---- leaders (cfg.py:63-70); block_of doubles as the leader flag array first ----
+  for (uint32_t i = 0; i < n; ++i) block_of[i] = 0;
+  block_of[0] = 1;
+  for (uint32_t i = 0; i < L; ++i) {
+    const uint32_t s = lt.find(lab[i].hash);
+    if (lt.last[s] == i && lab[i].index < n) block_of[lab[i].index] = 1;     // effective definition only
+  }
+  for (uint32_t i = 0; i + 1 < n; ++i) {
+    const uint32_t m = ins[i].meta;
+    const uint32_t base = ffb_meta_base(m);
+    if (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT) block_of[i + 1] = 1;
+  }
+  uint32_t nb = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (block_of[i]) block_start[nb++] = i;
+    block_of[i] = nb - 1;
+  }
+  block_start[nb] = n;
+  // ---- edges (cfg.py:80-92) and branch-target validation (ptx.py:277-284) ----
+  uint32_t n_edges = 0;
+  for (uint32_t b = 0; b < nb; ++b) { succ0[b] = -1; succ1[b] = -1; pred_ptr[b] = 0; }
+  pred_ptr[nb] = 0;
+  for (uint32_t i = 0; i < n && status == FFB_OK; ++i) {
+    const uint32_t m = ins[i].meta;
+    if (ffb_meta_cls(m) != FFB_CLS_BRANCH) continue;
+    const uint64_t tgt = ins[i].aux;
+    const uint32_t s = tgt ? lt.find(ffb_op_hash(tgt)) : lt.cap;
+    if (s == lt.cap) status = FFB_E_MALFORMED_PTX;
+  }
+  if (status != FFB_OK) { a.status[k] = status; if (a.flow) a.flow[k] = fi; return; }
+  for (uint32_t b = 0; b < nb; ++b) {
+    const FfbInsRec& last = ins[block_start[b + 1] - 1];
+    const uint32_t m = last.meta;
+    const uint32_t base = ffb_meta_base(m);
+    if (ffb_meta_cls(m) == FFB_CLS_BRANCH) {
+      const uint32_t s = lt.find(ffb_op_hash(last.aux));
+      const uint32_t tidx = lab[lt.last[s]].index;
+      if (tidx < n) succ0[b] = (int32_t)block_of[tidx];
+      if (ffb_meta_has_pred(m) && b + 1 < nb) succ1[b] = (int32_t)(b + 1);
+    } else if (base == FFB_BASE_RET || base == FFB_BASE_EXIT) {
+    } else if (b + 1 < nb) {
+      succ1[b] = (int32_t)(b + 1);
+    }
+    if (succ0[b] >= 0) { ++n_edges; ++pred_ptr[succ0[b] + 1]; }
+    if (succ1[b] >= 0) { ++n_edges; ++pred_ptr[succ1[b] + 1]; }
+  }
+  for (uint32_t b = 0; b < nb; ++b) pred_ptr[b + 1] += pred_ptr[b];
+  for (uint32_t b = 0; b < nb; ++b) mark[b] = pred_ptr[b];           // fill cursors
+  for (uint32_t b = 0; b < nb; ++b) {                                // edge order = (b, branch) then (b, fallthrough)
+    if (succ0[b] >= 0) pred_list[mark[succ0[b]]++] = b;
+    if (succ1[b] >= 0) pred_list[mark[succ1[b]]++] = b;
+  }
+  // ---- reverse post-order from block 0 (iterative DFS) ----
+  for (uint32_t b = 0; b < nb; ++b) { rpo_num[b] = -1; mark[b] = 0; idom[b] = -1; }
+  uint32_t post = 0, sp = 0;
+  stack[sp++] = 0; mark[0] = 1;            // mark: 0 unseen, 1 = next child is succ0, 2 = succ1, 3 = done
+  while (sp) {
+    const uint32_t b = stack[sp - 1];
+    int32_t child = -1;
+    while (mark[b] < 3 && child < 0) {
+      const int32_t c = mark[b] == 1 ? succ0[b] : succ1[b];
+      ++mark[b];
+      if (c >= 0 && mark[c] == 0) child = c;
+    }
+    if (child >= 0) { mark[child] = 1; stack[sp++] = (uint32_t)child; }
+    else { rpo_order[post++] = b; --sp; }
+  }
+  const uint32_t n_reach = post;
+  for (uint32_t i = 0; i < n_reach; ++i) rpo_num[rpo_order[i]] = (int32_t)(n_reach - 1 - i);   // 0 = entry
+  // ---- immediate dominators (Cooper-Harvey-Kennedy) ----
+  idom[0] = 0;
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (int32_t r = (int32_t)n_reach - 2; r >= 0; --r) {            // reverse post-order, entry skipped
+      const uint32_t b = rpo_order[r];
+      int32_t nd = -1;
+      for (uint32_t p = pred_ptr[b]; p < pred_ptr[b + 1]; ++p) {
+        const uint32_t q = pred_list[p];
+        if (rpo_num[q] < 0 || idom[q] < 0) continue;
+        if (nd < 0) { nd = (int32_t)q; continue; }
+        int32_t x = (int32_t)q, y = nd;
+        while (x != y) {
+          while (rpo_num[x] > rpo_num[y]) x = idom[x];
+          while (rpo_num[y] > rpo_num[x]) y = idom[y];
+        }
+        nd = x;
+      }
+      if (nd != idom[b]) { idom[b] = nd; changed = true; }
+    }
+  }
+  // ---- natural loops, one per header in ascending header order (cfg.py:124-151) ----
+  for (uint32_t b = 0; b < nb; ++b) { weight[b] = 1.0; mark[b] = 0; }
+  uint32_t n_loops = 0;
+  for (uint32_t h = 0; h < nb; ++h) {
+    // back edges into h: predecessors u with h in dom(u)
+    bool is_header = false;
+    const uint32_t stamp = h + 1;
+    for (uint32_t p = pred_ptr[h]; p < pred_ptr[h + 1]; ++p) {
+      const uint32_t u = pred_list[p];
+      if (!dominates(idom, rpo_num, h, u)) continue;
+      is_header = true;
+      // body = {h, u} + everything that reaches u without passing h
+      mark[h] = stamp;
+      if (mark[u] != stamp) { mark[u] = stamp; }
+      uint32_t top = 0;
+      stack[top++] = u;
+      while (top) {
+        const uint32_t x = stack[--top];
+        if (x == h) continue;
+        for (uint32_t q = pred_ptr[x]; q < pred_ptr[x + 1]; ++q) {
+          const uint32_t y = pred_list[q];
+          if (mark[y] != stamp) { mark[y] = stamp; stack[top++] = y; }
+        }
+      }
+    }
+    if (!is_header) continue;
+    const uint32_t h0 = block_start[h];
+    // header label: the dictionary's last name that maps to the header's first instruction
+    uint64_t hl_hash = 0; uint32_t hl_off = 0; bool hl_any = false; uint32_t hl_order = 0;
+    for (uint32_t i = 0; i < L; ++i) {
+      const uint32_t s = lt.find(lab[i].hash);
+      if (lt.last[s] != i || lab[i].index != h0) continue;       // only effective definitions
+      const uint32_t ord = lt.first[s];
+      if (!hl_any || ord >= hl_order) { hl_any = true; hl_order = ord; hl_hash = lab[i].hash; hl_off = lab[lt.first[s]].off; }
+    }
+    // ---- trip count ----
+    double trip = -1.0;
+    bool annotated = false;
+    if (hl_any) {
+      for (int q = 0; q < a.n_ann; ++q)
+        if (a.ann_hash[q] == hl_hash) { trip = a.ann_trip[q]; annotated = true; if (a.ann_hit) a.ann_hit[q] = 1; }
+    }
+    if (!annotated) {
+      // cfg.py:191-279
+      bool ok = true;
+      int64_t latch = -1;
+      for (uint32_t b = 0; b < nb; ++b) {
+        if (mark[b] != stamp) continue;
+        for (uint32_t i = block_start[b]; i < block_start[b + 1]; ++i) {
+          const uint32_t m = ins[i].meta;
+          if (ffb_meta_cls(m) == FFB_CLS_BRANCH && ffb_meta_has_pred(m)) {
+            const uint32_t s = lt.find(ffb_op_hash(ins[i].aux));
+            if (lab[lt.last[s]].index == h0) latch = i;
+          }
+        }
+      }
+      int64_t cmp_i = -1;
+      if (latch < 0) ok = false;
+      if (ok) {
+        const uint64_t preg = ins[latch].pred;
+        for (uint32_t b = 0; b < nb; ++b) {
+          if (mark[b] != stamp) continue;
+          for (uint32_t i = block_start[b]; i < block_start[b + 1]; ++i) {
+            const uint32_t m = ins[i].meta;
+            if (ffb_meta_base(m) == FFB_BASE_SETP && ffb_meta_nops(m) >= 1 && ffb_op_kind(ins[i].op[0]) != FFB_OPK_INT &&
+                ffb_op_hash(ins[i].op[0]) == preg) cmp_i = i;
+          }
+        }
+        if (cmp_i < 0 || ffb_meta_nops(ins[cmp_i].meta) < 3) ok = false;
+      }
+      uint64_t counter = 0; int64_t bound = 0; uint32_t rel = FFB_CMP_NONE;
+      if (ok) {
+        const FfbInsRec& c = ins[cmp_i];
+        counter = c.op[1];
+        if (!starts_with_percent(counter)) ok = false;
+        if (ok && ffb_op_kind(c.op[2]) == FFB_OPK_BIGINT) { ok = false; status = FFB_E_CAPACITY; }
+        if (ok && ffb_op_kind(c.op[2]) != FFB_OPK_INT) ok = false;
+        if (ok) bound = ffb_op_int(c.op[2]);
+        rel = ffb_meta_cmp(c.meta);
+        if (rel == FFB_CMP_NONE) ok = false;
+        if (ok && ffb_meta_pred_neg(ins[latch].meta)) {
+          const uint32_t inv[7] = {0, FFB_CMP_GE, FFB_CMP_LT, FFB_CMP_GT, FFB_CMP_LE, FFB_CMP_NE, FFB_CMP_EQ};
+          rel = inv[rel];
+        }
+      }
+      int64_t stride = 0; bool have_stride = false;
+      if (ok) {
+        const uint64_t ch = ffb_op_hash(counter);
+        for (uint32_t b = 0; b < nb && ok; ++b) {
+          if (mark[b] != stamp) continue;
+          for (uint32_t i = block_start[b]; i < block_start[b + 1] && ok; ++i) {
+            const uint32_t m = ins[i].meta;
+            const uint32_t base = ffb_meta_base(m);
+            if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && ffb_meta_nops(m) == 3 &&
+                starts_with_percent(ins[i].op[0]) && ffb_op_hash(ins[i].op[0]) == ch &&
+                starts_with_percent(ins[i].op[1]) && ffb_op_hash(ins[i].op[1]) == ch) {
+              if (ffb_op_kind(ins[i].op[2]) == FFB_OPK_BIGINT) { ok = false; status = FFB_E_CAPACITY; break; }
+              if (ffb_op_kind(ins[i].op[2]) != FFB_OPK_INT) { ok = false; break; }
+              const int64_t imm = ffb_op_int(ins[i].op[2]);
+              if (have_stride) { ok = false; break; }
+              stride = base == FFB_BASE_SUB ? -imm : imm;
+              have_stride = true;
+            }
+          }
+        }
+        if (ok && (!have_stride || stride == 0)) ok = false;
+      }
+      int64_t init = 0; bool have_init = false;
+      if (ok) {
+        const uint64_t ch = ffb_op_hash(counter);
+        for (uint32_t i = 0; i < h0; ++i) {
+          const uint32_t m = ins[i].meta;
+          if (ffb_meta_nops(m) == 0) continue;
+          const uint64_t d0 = ins[i].op[0];
+          if (!starts_with_percent(d0) || ffb_op_hash(d0) != ch) continue;
+          have_init = false;
+          if (ffb_meta_base(m) == FFB_BASE_MOV && ffb_meta_nops(m) == 2) {
+            if (ffb_op_kind(ins[i].op[1]) == FFB_OPK_INT) { init = ffb_op_int(ins[i].op[1]); have_init = true; }
+            else if (ffb_op_kind(ins[i].op[1]) == FFB_OPK_BIGINT) status = FFB_E_CAPACITY;
+          }
+        }
+        if (!have_init) ok = false;
+      }
+      if (ok) {
+        // cfg.py:259-279, Python int arithmetic: "/" is true division, then ceil / floor
+        double trips = 0.0;
+        const double span_up = (double)(bound - init), span_dn = (double)(init - bound);
+        if (rel == FFB_CMP_LT && stride > 0) trips = ceil(span_up / (double)stride);
+        else if (rel == FFB_CMP_LE && stride > 0) trips = floor(span_up / (double)stride) + 1.0;
+        else if (rel == FFB_CMP_GT && stride < 0) trips = ceil(span_dn / (double)(-stride));
+        else if (rel == FFB_CMP_GE && stride < 0) trips = floor(span_dn / (double)(-stride)) + 1.0;
+        else if (rel == FFB_CMP_NE) {
+          const int64_t span = bound - init;
+          if (span % stride == 0 && span / stride > 0) trips = (double)(span / stride);
+          else ok = false;
+        } else ok = false;
+        if (ok) trip = trips < 1.0 ? 1.0 : trips;
+      }
+      if (!ok) trip = a.default_trip;
+    }
+    if (!(trip > 1.0)) trip = 1.0;                                  // cfg.py:181 max(1.0, trip)
+    uint32_t n_body = 0;
+    for (uint32_t b = 0; b < nb; ++b)
+      if (mark[b] == stamp) { weight[b] *= trip; ++n_body; }       // cfg.py:52-53
+    if (a.out_loops) {
+      FfbLoopRec lr;
+      lr.header = h; lr.n_body = n_body; lr.trip = trip; lr.label_hash = hl_any ? hl_hash : 0;
+      lr.label_off = hl_off; lr.has_label = hl_any ? 1u : 0u;
+      a.out_loops[o1 + n_loops] = lr;
+      if (a.out_loop_body && (int64_t)(n_loops + 1) * nb <= a.loop_body_cap)
+        for (uint32_t b = 0; b < nb; ++b) a.out_loop_body[(int64_t)n_loops * nb + b] = mark[b] == stamp ? 1 : 0;
+    }
+    ++n_loops;
+  }
+  // ---- one textual pass: affine scales, aligned fraction, dynamic counts ----
+  st.clear();
+  double n_mem = 0.0, mem_bytes = 0.0, u_fp = 0.0, u_int = 0.0, u_sfu = 0.0, u_alu = 0.0, n_sync = 0.0;
+  double al_hit = 0.0, al_tot = 0.0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const FfbInsRec r = ins[i];
+    const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m), base = ffb_meta_base(m);
+    const double wgt = weight[block_of[i]];
+    const bool is_mem = cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE;
+    if (is_mem) {
+      const uint32_t space = ffb_meta_space(m), bytes = ffb_meta_bytes(m);
+      if (space != FFB_SP_PARAM) { n_mem += wgt; mem_bytes += wgt * (double)bytes; }      // features.py:72-75
+      if (space == FFB_SP_GLOBAL) {                                                      // alignment.py:137-144
+        int64_t sc = kNoneScale;
+        const uint32_t ak = ffb_meta_addr(m);
+        if (ak == FFB_ADDR_SYMBOL) sc = 0;
+        else if (ak == FFB_ADDR_REG) sc = st.get(ffb_op_hash(r.aux));
+        al_tot += wgt;
+        if (sc_known(sc) && sc != kBigScale && (sc < 0 ? -sc : sc) == (int64_t)bytes) al_hit += wgt;
+      }
+      if (cls == FFB_CLS_MEMLOAD && nops >= 1 && ffb_meta_dst_reg(m))                    // alignment.py:84-88
+        st.put(ffb_op_hash(r.op[0]), space == FFB_SP_PARAM ? 0 : kNoneScale);
+      continue;
+    }
+    if (cls == FFB_CLS_FP32) u_fp += wgt;
+    else if (cls == FFB_CLS_INT) u_int += wgt;
+    else if (cls == FFB_CLS_SFU) u_sfu += wgt;
+    else if (cls == FFB_CLS_ALU) u_alu += wgt;
+    else if (cls == FFB_CLS_SYNC) n_sync += wgt;
+    if (nops == 0 || !ffb_meta_dst_reg(m)) continue;                                      // alignment.py:91-95
+    const uint64_t dst = ffb_op_hash(r.op[0]);
+    int64_t v;
+    if (base == FFB_BASE_MOV && nops == 2) v = operand_scale(r.op[1], st);
+    else if ((base == FFB_BASE_CVT || base == FFB_BASE_CVTA) && nops >= 2) {
+      // scale of the LAST operand
+      uint64_t lastd = nops == 2 ? r.op[1] : nops == 3 ? r.op[2] : nops == 4 ? r.op[3] : r.aux;
+      if (nops > 5) { status = FFB_E_CAPACITY; lastd = 0; }
+      v = operand_scale(lastd, st);
+    } else if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && nops == 3) {
+      const int64_t x = operand_scale(r.op[1], st), y = operand_scale(r.op[2], st);
+      v = base == FFB_BASE_ADD ? sc_add(x, y) : sc_add(x, sc_neg(y));
+    } else if (base == FFB_BASE_MUL && nops == 3) v = mul_scale(r.op[1], r.op[2], st);
+    else if ((base == FFB_BASE_MAD || base == FFB_BASE_FMA) && nops == 4) v = sc_add(mul_scale(r.op[1], r.op[2], st), operand_scale(r.op[3], st));
+    else if (base == FFB_BASE_SHL && nops == 3) {
+      const int64_t x = operand_scale(r.op[1], st);
+      if (!sc_known(x) || !is_int_lit(r.op[2])) v = kNoneScale;
+      else {
+        const int64_t sh = int_as_scale(r.op[2]);
+        if (sh == kBigScale || sh < 0) { status = FFB_E_CAPACITY; v = kNoneScale; }   // 1 << huge / negative: reference raises
+        else v = x == 0 ? 0 : (sh >= 61 ? kBigScale : sc_mul(x, (int64_t)1 << sh));
+      }
+    } else if (base == FFB_BASE_SETP) continue;
+    else {
+      // unmodelled producer: uniform only if it has sources and all of them are uniform
+      bool all0 = nops >= 2;
+      for (uint32_t q = 1; q < nops && q < 4 && all0; ++q) all0 = operand_scale(r.op[q], st) == 0;
+      if (all0 && nops >= 5) all0 = operand_scale(r.aux, st) == 0;
+      if (all0 && nops >= 6 && ffb_meta_extra_reg(m)) { status = FFB_E_CAPACITY; all0 = false; }
+      v = all0 ? 0 : kNoneScale;
+    }
+    st.put(dst, v);
+  }
+  feat[FFB_F_N_MEM] = n_mem; feat[FFB_F_MEM_BYTES] = mem_bytes;
+  feat[FFB_F_FP32] = u_fp; feat[FFB_F_INT] = u_int; feat[FFB_F_SFU] = u_sfu; feat[FFB_F_ALU] = u_alu;
+  feat[FFB_F_N_SYNC] = n_sync;
+  feat[FFB_F_ALIGNED] = al_tot == 0.0 ? 1.0 : al_hit / al_tot;                            // alignment.py:145-147
+  feat[FFB_F_STATIC_SHARED] = (double)inf.static_shared;
+  feat[FFB_F_REGS_DECLARED] = (double)inf.regs_declared;
+  feat[FFB_F_N_INSTR] = (double)n;
+  a.status[k] = status;
+  fi.n_blocks = nb; fi.n_edges = n_edges; fi.n_loops = n_loops;
+  if (a.flow) a.flow[k] = fi;
+  if (a.out_block_start) for (uint32_t b = 0; b <= nb; ++b) a.out_block_start[o1 + b] = block_start[b];
+  if (a.out_weights) for (uint32_t b = 0; b < nb; ++b) a.out_weights[o1 + b] = weight[b];
+  if (a.out_edges) {
+    uint32_t e = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      if (succ0[b] >= 0) { a.out_edges[2 * (2 * o1 + e)] = (int32_t)b; a.out_edges[2 * (2 * o1 + e) + 1] = succ0[b]; ++e; }
+      if (succ1[b] >= 0) { a.out_edges[2 * (2 * o1 + e)] = (int32_t)b; a.out_edges[2 * (2 * o1 + e) + 1] = succ1[b]; ++e; }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, void* stream_) {
+  if (!ctx || !d || d->n_segs < 0 || !d->d_info || !d->d_ins_base || !d->d_lab_base || !d->d_ins || !d->d_labels ||
+      !d->d_feat || !d->d_status || d->n_ins_total < 0 || d->n_lab_total < 0)
+    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_kernel_features: bad argument");
+  if (d->n_segs == 0) return FFB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  FFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int64_t K = d->n_segs, N = d->n_ins_total, L = d->n_lab_total;
+  const size_t n1 = (size_t)(N + 2 * K + 8);       // block-indexed arrays
+  const size_t nL = (size_t)(2 * L + 4 * K + 8), nS = (size_t)(2 * N + 4 * K + 8);
+  size_t bytes = 0;
+  auto take = [&](size_t count, size_t elem) { size_t off = bytes; bytes += (count * elem + 15) & ~(size_t)15; return off; };
+  const size_t o_block_of = take((size_t)N + 8, 4), o_bstart = take(n1, 4), o_s0 = take(n1, 4), o_s1 = take(n1, 4),
+               o_pp = take(n1, 4), o_pl = take(2 * n1, 4), o_rn = take(n1, 4), o_ro = take(n1, 4), o_id = take(n1, 4),
+               o_mk = take(n1, 4), o_sk = take(n1, 4), o_w = take(n1, 8), o_lk = take(nL, 8), o_lf = take(nL, 4),
+               o_ll = take(nL, 4), o_sk2 = take(nS, 8), o_sv = take(nS, 8),
+               o_ah = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8), o_at = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8);
+  int32_t rc = ffb_reserve(ctx, &ctx->d_flow, bytes);
+  if (rc) return rc;
+  char* base = (char*)ctx->d_flow.p;
+  FlowArgs a = {};
+  a.n_segs = K; a.info = d->d_info; a.ins_base = d->d_ins_base; a.lab_base = d->d_lab_base;
+  a.ins = (const FfbInsRec*)d->d_ins; a.labels = (const FfbLabelRec*)d->d_labels; a.order = d->d_order;
+  a.default_trip = d->default_trip;
+  a.n_ann = d->n_ann > 0 ? d->n_ann : 0; a.ann_hit = d->d_ann_hit;
+  a.feat = d->d_feat; a.status = d->d_status; a.flow = d->d_flow;
+  a.block_of = (uint32_t*)(base + o_block_of); a.block_start = (uint32_t*)(base + o_bstart);
+  a.succ0 = (int32_t*)(base + o_s0); a.succ1 = (int32_t*)(base + o_s1);
+  a.pred_ptr = (uint32_t*)(base + o_pp); a.pred_list = (uint32_t*)(base + o_pl);
+  a.rpo_num = (int32_t*)(base + o_rn); a.rpo_order = (uint32_t*)(base + o_ro); a.idom = (int32_t*)(base + o_id);
+  a.mark = (uint32_t*)(base + o_mk); a.stack = (uint32_t*)(base + o_sk); a.weight = (double*)(base + o_w);
+  a.lab_key = (uint64_t*)(base + o_lk); a.lab_first = (uint32_t*)(base + o_lf); a.lab_last = (uint32_t*)(base + o_ll);
+  a.sc_key = (uint64_t*)(base + o_sk2); a.sc_val = (int64_t*)(base + o_sv);
+  a.ann_hash = (const uint64_t*)(base + o_ah); a.ann_trip = (const double*)(base + o_at);
+  if (a.n_ann > 0) {
+    if (!d->h_ann_hash || !d->h_ann_trip) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_kernel_features: annotation arrays missing");
+    rc = ffb_stage_reserve(ctx, (size_t)a.n_ann * 16);
+    if (rc) return rc;
+    memcpy(ctx->h_stage, d->h_ann_hash, (size_t)a.n_ann * 8);
+    memcpy((char*)ctx->h_stage + (size_t)a.n_ann * 8, d->h_ann_trip, (size_t)a.n_ann * 8);
+    FFB_CUDA(ctx, cudaMemcpyAsync(base + o_ah, ctx->h_stage, (size_t)a.n_ann * 8, cudaMemcpyHostToDevice, stream));
+    FFB_CUDA(ctx, cudaMemcpyAsync(base + o_at, (char*)ctx->h_stage + (size_t)a.n_ann * 8, (size_t)a.n_ann * 8, cudaMemcpyHostToDevice, stream));
+    FFB_CUDA(ctx, cudaEventRecord(ctx->stage_free, stream));
+    ctx->stage_busy = true;
+  }
+  a.out_block_start = d->d_block_start; a.out_edges = d->d_edges; a.out_loops = d->d_loops;
+  a.out_loop_body = d->d_loop_body; a.loop_body_cap = d->loop_body_cap; a.out_weights = d->d_weights;
+  const int64_t ctas = (K + kFlowThreads - 1) / kFlowThreads;
+  FFB_LAUNCH(flow_kernel, (unsigned)ctas, kFlowThreads, 0, stream, a);
+  return ffb_check_launch(ctx, "flow_kernel");
+}
+
+// Name hash used for annotation keys (same function as the lexer's label hash).
+extern "C" uint64_t ffb_name_hash(const uint8_t* name, int64_t len) {
+  uint64_t h = kFnvBasis;
+  for (int64_t i = 0; i < len; ++i) h = ffb_hash_step(h, name[i]);
+  return ffb_hash_fold(h);
+}

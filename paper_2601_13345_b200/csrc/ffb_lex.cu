@@ -309,7 +309,7 @@ FFB_D uint64_t describe_operand(const uint8_t* s, int a, int b) {
     bool uni = span_ends(s, a, b, "%gridid", 7) || span_ends(s, a, b, "WARP_SZ", 7);
     if (!uni && b - a >= 2 && s[b - 2] == '.' && (s[b - 1] == 'x' || s[b - 1] == 'y' || s[b - 1] == 'z'))
       uni = span_ends(s, a, b - 2, "%ctaid", 6) || span_ends(s, a, b - 2, "%nctaid", 7) || span_ends(s, a, b - 2, "%ntid", 5);
-    return ffb_op_make(uni ? FFB_OPK_UNIFORM : FFB_OPK_REG, h);
+    return ffb_op_make(uni ? FFB_OPK_UNIFORM_REG : FFB_OPK_REG, h);
   }
   int64_t v = 0;
   const int lit = py_int_literal(s, a, b, &v);

@@ -38,6 +38,7 @@ enum : uint64_t {
   FFB_OPK_UNIFORM = 4,   // uniform special or any non-% operand -> scale 0 (alignment.py:38-47)
   FFB_OPK_INT = 5,       // Python int(text, 0) literal, |v| < 2^60       (scale 0, value kept)
   FFB_OPK_BIGINT = 6,    // int literal outside that range
+  FFB_OPK_UNIFORM_REG = 7,  // %-prefixed uniform special (%ctaid.x, %ntid.y, %gridid ...) -> scale 0
 };
 FFB_HD uint64_t ffb_op_make(uint64_t kind, uint64_t payload) { return (kind << 61) | (payload & 0x1fffffffffffffffull); }
 FFB_HD uint64_t ffb_op_kind(uint64_t d) { return d >> 61; }

@@ -1,0 +1,80 @@
+"""K1 (lexer / classifier / histogram) and K1b (CFG, trips, alignment, dynamic counts)
+against the oracle: bit-exact histograms, declarations, statuses and feature rows."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import flipflop_oracle as orc
+from edge_cases import EDGE_CASES
+from paper_2601_13345_b200 import corpus, native, synth
+
+STATUS_OF = {"MalformedPtx": 1, "NoKernelFound": 2}
+
+
+def _corpus(texts):
+    blobs = [t.encode("ascii") for t in texts]
+    offs = np.cumsum([0] + [len(b) for b in blobs])
+    return corpus.upload_corpus(b"".join(blobs), offs)
+
+
+def _check(texts, default_trip=32.0):
+    corp = _corpus(texts)
+    lex, fl = corpus.analyze_corpus(corp, default_trip=default_trip)
+    info, hist = lex.info_np(), lex.hist.cpu().numpy()
+    feat, status = fl.feat.cpu().numpy(), fl.status.cpu().numpy()
+    for k, src in enumerate(texts):
+        try:
+            kern = orc.parse_kernel(src)
+            want_row = np.asarray(orc.kernel_feature_row(src, default_trip=default_trip), dtype=np.float64)
+            want_status = 0
+        except orc.OracleError as ex:
+            want_status = STATUS_OF[ex.kind]
+        assert int(status[k]) == want_status, (k, src[:60])
+        if want_status:
+            continue
+        assert hist[k].tolist() == orc.class_histogram(kern)
+        assert int(info[k]["n_instr"]) == len(kern.ins)
+        assert int(info[k]["static_shared"]) == kern.shared
+        assert int(info[k]["regs_declared"]) == sum(kern.regs.values())
+        name = src.encode()[int(info[k]["name_off"]): int(info[k]["name_off"]) + int(info[k]["name_len"])].decode()
+        assert name == kern.name
+        assert feat[k, :11].tobytes() == want_row.tobytes(), (k, feat[k, :11].tolist(), want_row.tolist())
+
+
+def test_edge_cases(backend):
+    _check(list(EDGE_CASES.values()))
+
+
+@pytest.mark.parametrize("seed,default_trip", [(4, 32.0), (9, 7.5)])
+def test_synthetic_corpus(backend, seed, default_trip):
+    n = 16 if backend == "emul" else 600
+    text, offs = synth.ptx_corpus(seed=seed, n_kernels=n, lo=20, hi=700 if backend == "emul" else 5000)
+    _check([text[offs[i]:offs[i + 1]].decode("ascii") for i in range(n)], default_trip)
+
+
+def test_tile_boundaries(backend):
+    """Kernels longer than one 4 KB tile, long preambles, statements split over tile edges."""
+    rng = np.random.default_rng(5)
+    texts = []
+    for pad in (0, 1, 15, 16, 17, 2047, 3000, 4000, 4050, 4070):
+        body = "\n".join(f"\tadd.s32 \t%r{i % 7}, %r{(i + 1) % 7}, {i};  // note {i}" for i in range(int(rng.integers(150, 400))))
+        multi = "\tcall.uni (retval0),\n\tfoo,\n\t(\n\tparam0,\n\tparam1\n\t);\n"
+        texts.append("//" + "x" * pad + "\n.visible .entry t" + str(pad) + "(\n.param .u64 p0)\n{\n" + body + "\n" + multi * 3
+                     + "L:\n\t@%p1 bra L;\n\tret;\n}\n")
+    _check(texts)
+
+
+def test_named_kernel_selection(backend):
+    src = ".entry a()\n{\n ret;\n}\n.entry b()\n{\n add.s32 %r1, %r1, 1;\n exit;\n}\n"
+    corp = _corpus([src])
+    res = corpus.lex_histogram(corp, kernel_name="b")
+    assert int(res.info_np()[0]["status"]) == 0 and res.hist.cpu().numpy()[0].tolist() == orc.class_histogram(orc.parse_kernel(src, "b"))
+    res = corpus.lex_histogram(corp, kernel_name="zzz")
+    assert int(res.info_np()[0]["status"]) == 2
+
+
+def test_line_longer_than_tile_is_reported(backend):
+    src = ".entry a()\n{\n add.s32 %r1, %r1, " + "1" * 6000 + ";\n ret;\n}\n"
+    res = corpus.lex_histogram(_corpus([src]))
+    assert int(res.info_np()[0]["status"]) == 11       # FFB_E_CAPACITY, never a silent wrong answer
