@@ -82,7 +82,7 @@ enum FfbSpecCol {
 enum { FFB_D_MWP = 0, FFB_D_CWP, FFB_D_BW_EFF, FFB_D_T_MEM, FFB_D_T_COMP, FFB_D_T_SYNC, FFB_D_T_EXEC,
        FFB_D_P_UNITS, FFB_D_P_SHAPE, FFB_D_P_MEM, FFB_D_P_SM, FFB_D_P_DYN, FFB_D_F_ADJ, FFB_D_CI,
        FFB_D_ACTIVE_SMS, FFB_D_CAP_LIMITED, FFB_D_E_PRED, FFB_D_WARPS, FFB_D_BLOCKS_PER_SM,
-       FFB_D_ETA, FFB_DETAIL_WIDTH };
+       FFB_D_ETA, FFB_D_WAVES, FFB_DETAIL_WIDTH };
 
 /* flag bits of d_flags */
 enum { FFB_PT_VALID = 1, FFB_PT_CAP_LIMITED = 2 };
@@ -144,13 +144,18 @@ int32_t ffb_enumerate_shapes(const double* h_spec_row, int64_t shared_dyn,
  *   front of the eligible points, written as in-group indices ordered by
  *   (e, t, tie[idx]) — pass tie = rank of (block_x, block_y, cap) to reproduce
  *   explorer.py:113-119; NULL means the index itself.
- * d_front_idx [n_groups, cap_front]; d_front_n [n_groups] (true size, even if > cap_front,
- * in which case the status word gets FFB_E_CAPACITY); d_tpeak [n_groups] or NULL.
+ * Dense mode (d_front_off == NULL): d_front_idx [n_groups, cap_front].
+ * Compact mode (d_front_off != NULL): each group's run is appended to d_front_idx
+ * (cap_front = total entries available) at offset d_front_off[g]; runs of different groups
+ * land in launch-dependent order, each run itself is in reference order.
+ * d_front_n [n_groups] is always the true front size; when a front (dense) or the total
+ * (compact) does not fit, the status word gets bit FFB_E_CAPACITY.  d_tpeak [n_groups] or NULL.
  */
 int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const double* d_t,
                            int64_t n_groups, int64_t group_size, const uint32_t* d_tie,
                            double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
-                           double* d_tpeak, int64_t cap_front, uint32_t* d_status, void* stream);
+                           double* d_tpeak, int64_t cap_front, int64_t* d_front_off,
+                           uint32_t* d_status, void* stream);
 
 /* One large candidate set (BASELINE config 5).  Streaming cull against a sentinel
  * staircase, exact pass on the survivors.  Output: global indices (or d_id values when

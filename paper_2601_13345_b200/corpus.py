@@ -127,12 +127,12 @@ def lex_records(corp: Corpus, *, kernel_name: str | None = None, spans: bool = F
     K = corp.n_segs
     name = kernel_name.encode() if kernel_name else None
     res = lex_histogram(corp, kernel_name=kernel_name, rt=rt)
-    counts = res.info_i32()[:, 1:3].to(torch.int64)
-    incl = torch.cumsum(counts, dim=0)
-    base = (incl - counts).contiguous()
-    totals = incl[-1].cpu() if K else torch.zeros(2, dtype=torch.int64)
-    res.n_ins, res.n_lab = int(totals[0]), int(totals[1])
-    res.ins_base, res.lab_base = base[:, 0].contiguous(), base[:, 1].contiguous()
+    i32 = res.info_i32()
+    n_ins = i32[:, 1].to(torch.int64).contiguous()
+    n_lab = i32[:, 2].to(torch.int64).contiguous()
+    inc_i, inc_l = torch.cumsum(n_ins, dim=0), torch.cumsum(n_lab, dim=0)
+    res.ins_base, res.lab_base = (inc_i - n_ins).contiguous(), (inc_l - n_lab).contiguous()
+    res.n_ins, res.n_lab = (int(inc_i[-1]), int(inc_l[-1])) if K else (0, 0)
     res.ins = rt.empty((max(res.n_ins, 1), 64), torch.uint8)
     res.labels = rt.empty((max(res.n_lab, 1), 16), torch.uint8)
     res.spans = torch.zeros((max(res.n_ins, 1), 128), dtype=torch.uint8, device=rt.device) if spans else None
@@ -282,9 +282,11 @@ class BenchLexState:
         if not resident:
             corp.text.copy_(self.pin_host(), non_blocking=True)           # H2D inside the timed region
         _call_lex(rt, corp, lex.hist, lex.info)                           # K1 histogram + counts
-        counts = lex.info_i32()[:, 1:3].to(torch.int64)
-        base = (torch.cumsum(counts, dim=0) - counts)
-        lex.ins_base.copy_(base[:, 0]); lex.lab_base.copy_(base[:, 1])
+        i32 = lex.info_i32()
+        n_ins = i32[:, 1].to(torch.int64).contiguous()
+        n_lab = i32[:, 2].to(torch.int64).contiguous()
+        torch.sub(torch.cumsum(n_ins, dim=0), n_ins, out=lex.ins_base)
+        torch.sub(torch.cumsum(n_lab, dim=0), n_lab, out=lex.lab_base)
         _call_lex(rt, corp, lex.hist, lex.info, ins_base=lex.ins_base, lab_base=lex.lab_base, ins=lex.ins,
                   labels=lex.labels)                                      # K1 records
         kernel_features(corp, lex, out_feat=self.feat, rt=rt)             # K1b

@@ -233,7 +233,7 @@ predict_grid_kernel(GridArgs a) {
         d[FFB_D_F_ADJ] = a.tb.cap_fadj[(size_t)s * C + c]; d[FFB_D_CI] = ci;
         d[FFB_D_ACTIVE_SMS] = kr[KS_ACTIVE]; d[FFB_D_CAP_LIMITED] = limited ? 1.0 : 0.0;
         d[FFB_D_E_PRED] = e_pred; d[FFB_D_WARPS] = (double)warps; d[FFB_D_BLOCKS_PER_SM] = bps;
-        d[FFB_D_ETA] = eta;
+        d[FFB_D_ETA] = eta; d[FFB_D_WAVES] = waves;
       }
     }
   }

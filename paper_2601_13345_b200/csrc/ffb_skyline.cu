@@ -47,12 +47,15 @@ struct SkyArgs {
   int64_t group_size;
   double rho;               // <= 0: no floor
   int resident;             // points staged in shared memory
-  int surv_cap;             // survivor capacity (power of two)
+  int surv_cap;             // survivor capacity (entries of s_pm / s_gs)
+  int sort_cap;             // power of two >= surv_cap (entries of s_idx)
   // per-group outputs (optional)
   uint32_t* front_idx;
   uint32_t* front_n;
   double* tpeak;
   int64_t cap_front;
+  int64_t* front_off;       // optional: compact mode, offset of each group's run in front_idx
+  unsigned long long* front_total;   // compact mode: running total (atomic)
   // compact outputs (optional): appended at an atomically reserved offset
   double* out_e;
   double* out_t;
@@ -132,12 +135,12 @@ skyline_group_kernel(SkyArgs a) {
   const int G = (int)(rem < a.group_size ? rem : a.group_size);
   const int MC = a.surv_cap;
 
-  // shared-memory carve-up: [resident e,t] [sv_idx MC] [pm MC] [gs MC]
+  // shared-memory carve-up: [resident e,t] [pm MC] [idx sort_cap] [gs MC]
   double* s_e = reinterpret_cast<double*>(smem_raw);
   double* s_t = s_e + (a.resident ? a.group_size : 0);
   double* s_pm = s_t + (a.resident ? a.group_size : 0);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_pm + MC);
-  uint32_t* s_gs = s_idx + MC;
+  uint32_t* s_gs = s_idx + a.sort_cap;
 
   const double* ge = a.e + p0;
   const double* gt = a.t + p0;
@@ -293,11 +296,16 @@ skyline_group_kernel(SkyArgs a) {
   const uint32_t f = m > 0 ? s_gs[m - 1] : 0u;
   if (tid == 0) {
     if (a.front_n) a.front_n[g] = f;
-    if (a.front_idx && (int64_t)f > a.cap_front && a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
+    if (a.front_idx && !a.front_off && (int64_t)f > a.cap_front && a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
     if (a.out_count) s_base = atomicAdd(a.out_count, (unsigned long long)f);
+    if (a.front_off) {
+      s_base = atomicAdd(a.front_total, (unsigned long long)f);
+      a.front_off[g] = (int64_t)s_base;
+      if (s_base + f > (unsigned long long)a.cap_front && a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
+    }
   }
   __syncthreads();
-  const unsigned long long obase = a.out_count ? s_base : 0ull;
+  const unsigned long long obase = (a.out_count || a.front_off) ? s_base : 0ull;
   if (a.out_count && obase + f > (unsigned long long)a.out_cap) {
     if (tid == 0 && a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY);
   }
@@ -307,7 +315,8 @@ skyline_group_kernel(SkyArgs a) {
     if (incl != prev) {
       const uint32_t rank = prev;
       const uint32_t i = s_idx[p];
-      if (a.front_idx && (int64_t)rank < a.cap_front) a.front_idx[g * a.cap_front + rank] = i;
+      if (a.front_off) { if (obase + rank < (unsigned long long)a.cap_front) a.front_idx[obase + rank] = i; }
+      else if (a.front_idx && (int64_t)rank < a.cap_front) a.front_idx[g * a.cap_front + rank] = i;
       if (a.out_count && obase + rank < (unsigned long long)a.out_cap) {
         a.out_e[obase + rank] = pe[i];
         a.out_t[obase + rank] = pt[i];
@@ -317,27 +326,24 @@ skyline_group_kernel(SkyArgs a) {
   }
 }
 
-struct Plan { int resident; int surv_cap; size_t smem; };
+struct Plan { int resident; int surv_cap; int sort_cap; size_t smem; };
 
+// Survivor capacity = group size whenever shared memory allows, so a front made of ties
+// (every candidate on it) is still exact; two CTAs per SM stay resident for the 3248-point
+// groups of the headline workload (52 KB of points + 55 KB of survivor arrays).
 Plan plan_groups(const FfbContext* ctx, int64_t group_size) {
   Plan p;
-  int64_t mc = 1;
-  while (mc < group_size && mc < 2048) mc <<= 1;
-  if (mc < 32) mc = 32;
-  const size_t fixed = (size_t)mc * (8 + 4 + 4);
   const size_t limit = ctx->smem_optin ? ctx->smem_optin - 4096 : 96 * 1024;
-  const size_t budget2 = 100 * 1024;   // keeps two CTAs per SM resident
-  size_t res_bytes = (size_t)group_size * 16;
-  p.resident = (fixed + res_bytes <= limit) ? 1 : 0;
-  // grow the survivor capacity when shared memory is spare and the group is large
-  if (p.resident && fixed + res_bytes > budget2) {
-    while (mc < group_size && (size_t)(mc * 2) * 16 + res_bytes <= limit) mc <<= 1;
-  }
-  if (!p.resident) {
-    while (mc < group_size && (size_t)(mc * 2) * 16 <= limit) mc <<= 1;
-  }
-  p.surv_cap = (int)mc;
-  p.smem = (size_t)mc * 16 + (p.resident ? res_bytes : 0);
+  auto need = [](int64_t mc, bool resident, int64_t g) {
+    int64_t sc = 32; while (sc < mc) sc <<= 1;
+    return (size_t)(mc * 12 + sc * 4 + (resident ? g * 16 : 0) + 64);
+  };
+  int64_t mc = group_size < 32 ? 32 : group_size;
+  p.resident = need(mc, true, group_size) <= limit ? 1 : 0;
+  if (!p.resident) { while (mc > 1024 && need(mc, false, group_size) > limit) mc = mc / 2; }
+  int64_t sc = 32; while (sc < mc) sc <<= 1;
+  p.surv_cap = (int)mc; p.sort_cap = (int)sc;
+  p.smem = need(mc, p.resident != 0, group_size);
   return p;
 }
 
@@ -345,6 +351,7 @@ int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t
   Plan p = plan_groups(ctx, a.group_size);
   a.resident = p.resident;
   a.surv_cap = p.surv_cap;
+  a.sort_cap = p.sort_cap;
   if (n_groups > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "skyline: too many groups for one launch");
   FFB_CUDA(ctx, cudaFuncSetAttribute(skyline_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   FFB_LAUNCH(skyline_group_kernel, (unsigned)n_groups, kThreads, p.smem, stream, a);
@@ -356,8 +363,8 @@ int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t
 extern "C" int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const double* d_t,
                                       int64_t n_groups, int64_t group_size, const uint32_t* d_tie,
                                       double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
-                                      double* d_tpeak, int64_t cap_front, uint32_t* d_status,
-                                      void* stream) {
+                                      double* d_tpeak, int64_t cap_front, int64_t* d_front_off,
+                                      uint32_t* d_status, void* stream) {
   if (!ctx || !d_e || !d_t || n_groups < 0 || group_size <= 0 || group_size > 0x7fffffffLL || cap_front < 0)
     return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline_groups: bad argument");
   if (!(rho <= 1.0)) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline_groups: rho must be <= 1");
@@ -368,6 +375,13 @@ extern "C" int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const 
   a.n_total = n_groups * group_size; a.group_size = group_size; a.rho = rho;
   a.front_idx = d_front_idx; a.front_n = d_front_n; a.tpeak = d_tpeak; a.cap_front = cap_front;
   a.status = d_status;
+  if (d_front_off) {
+    int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 256);
+    if (rc) return rc;
+    a.front_off = d_front_off;
+    a.front_total = (unsigned long long*)ctx->d_sky.p;
+    FFB_CUDA(ctx, cudaMemsetAsync(a.front_total, 0, 8, (cudaStream_t)stream));
+  }
   return launch_groups(ctx, a, n_groups, (cudaStream_t)stream);
 }
 
@@ -408,8 +422,7 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   int which = 0;
   FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
   for (int level = 0; level < 64; ++level) {
-    // later levels may end early: one CTA can stream a modest set straight from L2
-    const bool last = cur_n <= chunk || (level > 0 && cur_n <= 32 * chunk);
+    const bool last = cur_n <= chunk;
     const int64_t n_groups = (cur_n + chunk - 1) / chunk;
     SkyArgs a = {};
     a.e = cur_e; a.t = cur_t; a.id = cur_id; a.tie = nullptr;

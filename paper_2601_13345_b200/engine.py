@@ -121,27 +121,39 @@ def enumerate_shapes(spec_row: np.ndarray, shared_dyn: int, dims, rt: native.Run
 
 def skyline_groups(e: torch.Tensor, t: torch.Tensor, n_groups: int, group_size: int, *,
                    tie: torch.Tensor | None = None, rho: float = 0.95, cap_front: int | None = None,
-                   check: bool = True, rt: native.Runtime | None = None):
-    """K4 on n_groups consecutive groups.  Returns (front_idx [n_groups, cap], front_n, t_peak)."""
+                   compact: bool = False, out: tuple | None = None, check: bool = True,
+                   rt: native.Runtime | None = None):
+    """K4 on n_groups consecutive groups.
+
+    Dense (default): returns (front_idx [n_groups, cap_front], front_n, t_peak).
+    ``compact=True``: returns (front_idx [cap_front] flat, front_n, t_peak, front_off) where group
+    g's front is front_idx[front_off[g] : front_off[g] + front_n[g]]; cap_front is the TOTAL capacity.
+    """
     rt = rt or native.get_runtime()
     assert e.dtype == torch.float64 and t.dtype == torch.float64 and e.is_contiguous() and t.is_contiguous()
     assert e.numel() == n_groups * group_size == t.numel()
     cap_front = int(cap_front if cap_front is not None else group_size)
-    front_idx = rt.empty((n_groups, cap_front), torch.int32)
-    front_n = rt.empty((n_groups,), torch.int32)
-    tpeak = rt.empty((n_groups,), torch.float64)
-    status = torch.zeros(1, dtype=torch.int32, device=rt.device)
+    if out is not None:
+        front_idx, front_n, tpeak, front_off = out
+    else:
+        front_idx = rt.empty((cap_front,) if compact else (n_groups, cap_front), torch.int32)
+        front_n = rt.empty((n_groups,), torch.int32)
+        tpeak = rt.empty((n_groups,), torch.float64)
+        front_off = rt.empty((n_groups,), torch.int64) if compact else None
+    status = torch.zeros(1, dtype=torch.int32, device=rt.device) if check else None
     if tie is not None:
         assert tie.dtype == torch.int32 and tie.numel() == group_size and tie.is_contiguous()
     rc = rt.lib.ffb_skyline_groups(rt.ctx, native.ptr(e), native.ptr(t), n_groups, group_size, native.ptr(tie),
                                    float(rho), native.ptr(front_idx), native.ptr(front_n), native.ptr(tpeak),
-                                   cap_front, native.ptr(status), rt.stream())
+                                   cap_front, native.ptr(front_off), native.ptr(status), rt.stream())
     rt.check(rc, "ffb_skyline_groups")
     if check:
         st = int(status.item()) & 0xFFFFFFFF
         for code in range(1, 32):
             if st & (1 << code):
                 raise_for_status(code, "skyline capacity exceeded (front or survivor buffer)")
+    if compact:
+        return front_idx, front_n, tpeak, front_off
     return front_idx, front_n, tpeak
 
 

@@ -22,13 +22,13 @@ FEAT_WIDTH = 18
  F_REGS_DECLARED, F_N_INSTR, F_RESERVED, F_OVR, F_OVR_WARPS, F_OVR_BPS, F_OVR_ETA, F_OVR_NCOMP,
  F_OVR_TEXEC) = range(18)
 SPEC_WIDTH = 48
-DETAIL_WIDTH = 20
+DETAIL_WIDTH = 21
 N_CLASSES = 9
 PT_VALID, PT_CAP_LIMITED = 1, 2
 
 (D_MWP, D_CWP, D_BW_EFF, D_T_MEM, D_T_COMP, D_T_SYNC, D_T_EXEC, D_P_UNITS, D_P_SHAPE, D_P_MEM,
  D_P_SM, D_P_DYN, D_F_ADJ, D_CI, D_ACTIVE_SMS, D_CAP_LIMITED, D_E_PRED, D_WARPS, D_BLOCKS_PER_SM,
- D_ETA) = range(DETAIL_WIDTH)
+ D_ETA, D_WAVES) = range(DETAIL_WIDTH)
 
 _vp, _i64, _i32, _f64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double
 
@@ -50,7 +50,7 @@ _SIGNATURES = {
     "ffb_launch_count": (_i64, [_vp]),
     "ffb_predict_grid": (_i32, [_vp, C.POINTER(GridDesc), _vp]),
     "ffb_enumerate_shapes": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_i64)]),
-    "ffb_skyline_groups": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "ffb_skyline_groups": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "ffb_lex_corpus": (_i32, [_vp, _vp, _vp]),
     "ffb_kernel_features": (_i32, [_vp, _vp, _vp]),
     "ffb_name_hash": (C.c_uint64, [C.c_char_p, _i64]),
