@@ -315,10 +315,10 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
-        k_cpu = min(K, 24 * workers)
+        k_cpu = min(K, 1000 * workers)
         pts, t_score, nb, t_lex = cpu_sample(feat_np, res_np, shp_xy, tie_np,
                                             corpus.host_sample() if corpus is not None else None,
-                                            workers, k_cpu, lex_bytes=3_000_000 * workers // 8)
+                                            workers, k_cpu, lex_bytes=2_500_000 * workers)
         cpu = {"value": pts / t_score, "unit": "configs/s", "cores": workers, "kind": "port",
                "sample": f"oracle (numpy score_grid + sort-sweep front) on {k_cpu} kernels x {G} configs = {pts} points, "
                          f"{workers} processes, {t_score:.1f} s"

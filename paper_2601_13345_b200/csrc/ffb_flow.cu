@@ -58,10 +58,10 @@ struct FlowArgs {
   uint32_t* mark;
   uint32_t* stack;
   double* weight;               // [N + 2K]
-  uint64_t* lab_key;            // [2L + 4K]
+  uint64_t* lab_key;            // [4L + 8K]
   uint32_t* lab_first;
   uint32_t* lab_last;
-  uint64_t* sc_key;             // [2N + 4K]
+  uint64_t* sc_key;             // [4N + 8K]
   int64_t* sc_val;
   // detail outputs (optional)
   uint32_t* out_block_start;
@@ -73,7 +73,8 @@ struct FlowArgs {
 };
 
 // ---- tiny open-addressing tables ----------------------------------------------------------------
-FFB_D uint32_t slot_of(uint64_t h, uint32_t cap) { return (uint32_t)((h * 0x9E3779B97F4A7C15ull) >> 33) % cap; }
+// capacities are powers of two
+FFB_D uint32_t slot_of(uint64_t h, uint32_t cap) { return (uint32_t)((h * 0x9E3779B97F4A7C15ull) >> 33) & (cap - 1u); }
 
 struct LabelTable {
   uint64_t* key; uint32_t* first; uint32_t* last; uint32_t cap;
@@ -83,7 +84,7 @@ struct LabelTable {
     for (uint32_t n = 0; n < cap; ++n) {
       if (key[s] == 0) return cap;
       if (key[s] == h + 1) return s;
-      s = s + 1 == cap ? 0 : s + 1;
+      s = (s + 1) & (cap - 1u);
     }
     return cap;
   }
@@ -92,7 +93,7 @@ struct LabelTable {
     for (;;) {
       if (key[s] == 0) { key[s] = h + 1; first[s] = order; last[s] = order; return; }
       if (key[s] == h + 1) { last[s] = order; return; }
-      s = s + 1 == cap ? 0 : s + 1;
+      s = (s + 1) & (cap - 1u);
     }
   }
 };
@@ -105,7 +106,7 @@ struct ScaleTable {
     for (uint32_t n = 0; n < cap; ++n) {
       if (key[s] == 0) return kNoneScale;
       if (key[s] == h + 1) return val[s];
-      s = s + 1 == cap ? 0 : s + 1;
+      s = (s + 1) & (cap - 1u);
     }
     return kNoneScale;
   }
@@ -113,7 +114,7 @@ struct ScaleTable {
     uint32_t s = slot_of(h, cap);
     for (;;) {
       if (key[s] == 0 || key[s] == h + 1) { key[s] = h + 1; val[s] = v; return; }
-      s = s + 1 == cap ? 0 : s + 1;
+      s = (s + 1) & (cap - 1u);
     }
   }
 };
@@ -210,10 +211,11 @@ flow_kernel(FlowArgs a) {
   uint32_t* stack = a.stack + o1;
   double* weight = a.weight + o1;
   LabelTable lt;
-  lt.key = a.lab_key + 2 * lb + 4 * k; lt.first = a.lab_first + 2 * lb + 4 * k; lt.last = a.lab_last + 2 * lb + 4 * k;
-  lt.cap = 2 * L + 3;
+  lt.key = a.lab_key + 4 * lb + 8 * k; lt.first = a.lab_first + 4 * lb + 8 * k; lt.last = a.lab_last + 4 * lb + 8 * k;
+  lt.cap = 4; while (lt.cap < 2 * L + 2) lt.cap <<= 1;          // <= 4L + 8
   ScaleTable st;
-  st.key = a.sc_key + 2 * ib + 4 * k; st.val = a.sc_val + 2 * ib + 4 * k; st.cap = 2 * n + 3;
+  st.key = a.sc_key + 4 * ib + 8 * k; st.val = a.sc_val + 4 * ib + 8 * k;
+  st.cap = 4; while (st.cap < 2 * n + 2) st.cap <<= 1;          // <= 4n + 8
 
   // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
   lt.clear();
@@ -418,16 +420,17 @@ flow_kernel(FlowArgs a) {
       int64_t init = 0; bool have_init = false;
       if (ok) {
         const uint64_t ch = ffb_op_hash(counter);
-        for (uint32_t i = 0; i < h0; ++i) {
+        // the LAST write before the header decides (cfg.py:246-254), so walk backwards and stop
+        for (int64_t i = (int64_t)h0 - 1; i >= 0; --i) {
           const uint32_t m = ins[i].meta;
           if (ffb_meta_nops(m) == 0) continue;
           const uint64_t d0 = ins[i].op[0];
           if (!starts_with_percent(d0) || ffb_op_hash(d0) != ch) continue;
-          have_init = false;
           if (ffb_meta_base(m) == FFB_BASE_MOV && ffb_meta_nops(m) == 2) {
             if (ffb_op_kind(ins[i].op[1]) == FFB_OPK_INT) { init = ffb_op_int(ins[i].op[1]); have_init = true; }
             else if (ffb_op_kind(ins[i].op[1]) == FFB_OPK_BIGINT) status = FFB_E_CAPACITY;
           }
+          break;
         }
         if (!have_init) ok = false;
       }
@@ -556,7 +559,7 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   FFB_CUDA(ctx, cudaSetDevice(ctx->device));
   const int64_t K = d->n_segs, N = d->n_ins_total, L = d->n_lab_total;
   const size_t n1 = (size_t)(N + 2 * K + 8);       // block-indexed arrays
-  const size_t nL = (size_t)(2 * L + 4 * K + 8), nS = (size_t)(2 * N + 4 * K + 8);
+  const size_t nL = (size_t)(4 * L + 8 * K + 16), nS = (size_t)(4 * N + 8 * K + 16);
   size_t bytes = 0;
   auto take = [&](size_t count, size_t elem) { size_t off = bytes; bytes += (count * elem + 15) & ~(size_t)15; return off; };
   const size_t o_block_of = take((size_t)N + 8, 4), o_bstart = take(n1, 4), o_s0 = take(n1, 4), o_s1 = take(n1, 4),

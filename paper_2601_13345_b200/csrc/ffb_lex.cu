@@ -35,6 +35,16 @@ constexpr uint8_t kNlInBlock = 0x8A;        // newline that sits inside a /* */ 
 
 enum Phase { PH_SEARCH = 0, PH_HEADER, PH_BODY, PH_DONE };
 
+// byte classes of the per-line feature scan
+enum { CC_WS = 1, CC_SEMI = 2, CC_LBRACE = 4, CC_RBRACE = 8, CC_COLON = 16, CC_LABEL = 32 };
+FFB_HD uint8_t char_class(unsigned c) {
+  return (uint8_t)((ffb_is_ws(c) ? CC_WS : 0) | (c == ';' ? CC_SEMI : 0) | (c == '{' ? CC_LBRACE : 0) |
+                   (c == '}' ? CC_RBRACE : 0) | (c == ':' ? CC_COLON : 0) | (ffb_is_label_char(c) ? CC_LABEL : 0));
+}
+// what the feature scan makes of a line (anything it cannot prove simple is LK_COMPLEX and
+// takes the general statement walk)
+enum { LK_BLANK = 0, LK_STMT, LK_LABEL, LK_SKIP, LK_COMPLEX };
+
 // comment automaton states
 enum { S_CODE = 0, S_SLASH, S_SLASH2, S_LINE, S_LINE_SLASH, S_BLK, S_BLK_STAR, S_LBLK, S_LBLK_STAR };
 
@@ -666,9 +676,12 @@ __global__ void __launch_bounds__(kWarps * 32)
 lex_corpus_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
+  __shared__ uint8_t s_cls[256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* s = smem_raw + (size_t)wid * kWarpSmem;
   uint16_t* nl = reinterpret_cast<uint16_t*>(s + kTile + kPad);
+  for (int c = threadIdx.x; c < 256; c += kWarps * 32) s_cls[c] = char_class((unsigned)c);
+  __syncthreads();
 
   for (;;) {
     unsigned long long w = 0;
@@ -834,12 +847,21 @@ lex_corpus_kernel(LexArgs a) {
               e = nl[li] & 0x7fff;
               if (b < pos) b = pos;               // the line that holds the opening brace
             }
-            // ---- brace depth and body end ----
+            // ---- feature scan: one uniform pass over the batch's lines ----
+            const int len = live ? e - b : 0;
+            int maxlen = len;
+#pragma unroll
+            for (int dd = 16; dd > 0; dd >>= 1) { const int o = __shfl_xor_sync(kFull, maxlen, dd); maxlen = o > maxlen ? o : maxlen; }
+            int fb = -1, lb = -1, n_semi = 0, n_colon = 0, n_labch = 0, n_nonws = 0;
             int run = 0, min_run = 0x7fffffff;
-            for (int i = b; i < e; ++i) {
-              const unsigned c = s[i];
-              if (c == '{') ++run;
-              else if (c == '}') { --run; if (run < min_run) min_run = run; }
+            for (int i = 0; i < maxlen; ++i) {
+              if (i < len) {
+                const unsigned k = s_cls[s[b + i]];
+                if (!(k & CC_WS)) { if (fb < 0) fb = b + i; lb = b + i; ++n_nonws; }
+                n_semi += (k >> 1) & 1; n_colon += (k >> 4) & 1; n_labch += (k >> 5) & 1;
+                if (k & CC_LBRACE) ++run;
+                else if (k & CC_RBRACE) { --run; if (run < min_run) min_run = run; }
+              }
             }
             int tot_delta = 0;
             const int d_in = depth + warp_excl_sum(run, &tot_delta);
@@ -857,11 +879,29 @@ lex_corpus_kernel(LexArgs a) {
               e = close_at;
             }
             const bool mine = live && lane <= end_lane;
-            // ---- pre-walk: structure of the line if it starts outside a statement ----
+            // ---- line kind ----
+            int kind = LK_COMPLEX;
+            if (fb < 0) kind = LK_BLANK;
+            else if (min_run == 0x7fffffff || (min_run >= 0 && run == 0)) {
+              const unsigned c_first = s[fb], c_last = s[lb];
+              if (c_first == '.') {
+                const bool decl = (s[fb + 1] == 'r' && s[fb + 2] == 'e' && s[fb + 3] == 'g') ||
+                                  (s[fb + 1] == 's' && s[fb + 2] == 'h' && s[fb + 3] == 'a');
+                if (n_semi == 0 && n_colon == 0 && !decl) kind = LK_SKIP;         // ptx.py:255-256
+              } else if (c_last == ';' && n_semi == 1 && n_colon == 0 && lb > fb) {
+                kind = LK_STMT;       // one statement, ';' last (braces inside operands are balanced)
+              } else if (c_last == ':' && n_semi == 0 && n_colon == 1 && n_labch == n_nonws - 1 && lb - fb + 1 == n_nonws && lb > fb) {
+                kind = LK_LABEL;                                                  // ptx.py:232-236
+              }
+            }
+            if (lane == end_lane) kind = LK_COMPLEX;
+            // ---- structure of the line if it starts outside a statement ----
             LineSummary sm;
-            sm.nonblank = sm.has_semi = sm.pend_out0 = sm.defer = sm.unterminated = false;
-            sm.n0 = sm.n_after = sm.lab0 = sm.lab_after = sm.dcl0 = sm.dcl_after = 0;
-            if (mine) sm = walk_line<0>(s, b, e, false, hi, d_in, at_seg_end, em);
+            sm.nonblank = kind != LK_BLANK; sm.has_semi = kind == LK_STMT;
+            sm.pend_out0 = sm.defer = sm.unterminated = false;
+            sm.n0 = kind == LK_STMT ? 1 : 0; sm.n_after = 0;
+            sm.lab0 = kind == LK_LABEL ? 1 : 0; sm.lab_after = 0; sm.dcl0 = sm.dcl_after = 0;
+            if (mine && kind == LK_COMPLEX) sm = walk_line<0>(s, b, e, false, hi, d_in, at_seg_end, em);
             // pending map: f0 = state after the line when it starts clean, f1 = when it starts
             // inside a statement; blank lines are the identity (ptx.py:230 `while line`)
             unsigned f0 = 0, f1 = 1;
@@ -897,7 +937,18 @@ lex_corpus_kernel(LexArgs a) {
               const int dcl0 = em.dcl_at;
               em.ins_at = ins0 + ins_ex; em.lab_at = lab0 + lab_ex; em.dcl_at = dcl0 + dcl_ex;
               em.line = line_no + (uint32_t)li;
-              if (run_line) walk_line<kMain>(s, b, e, p_in, hi, d_in, at_seg_end, em);
+              if (run_line) {
+                if (p_in || kind == LK_COMPLEX) walk_line<kMain>(s, b, e, p_in, hi, d_in, at_seg_end, em);
+                else if (kind == LK_STMT) do_statement<kMain>(s, fb, lb, em);
+                else if (kind == LK_LABEL) {
+                  if (kMain == 2) {
+                    FfbLabelRec L;
+                    L.hash = norm_hash(s, fb, lb); L.index = (uint32_t)(em.ins_at - a.ins_base[seg]);
+                    L.off = (uint32_t)(abase + fb - seg_begin);
+                    a.labels[em.lab_at] = L;
+                  }
+                }
+              }
               em.ins_at = ins0 + tot_ins; em.lab_at = lab0 + tot_lab; em.dcl_at = dcl0 + tot_dcl;
             }
             n_instr += (uint32_t)tot_ins; n_labels += (uint32_t)tot_lab; n_decls += (uint32_t)tot_dcl;

@@ -420,9 +420,13 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   const double* cur_e = d_e; const double* cur_t = d_t; const uint64_t* cur_id = d_id;
   int64_t cur_n = n;
   int which = 0;
+  bool stalled = false;
   FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
   for (int level = 0; level < 64; ++level) {
-    const bool last = cur_n <= chunk;
+    // normally the last level is one resident chunk; a set that stopped shrinking (its front is
+    // larger than a chunk, e.g. heavy ties) is finished by one CTA streaming from L2 with the
+    // largest survivor capacity shared memory allows
+    const bool last = cur_n <= chunk || stalled;
     const int64_t n_groups = (cur_n + chunk - 1) / chunk;
     SkyArgs a = {};
     a.e = cur_e; a.t = cur_t; a.id = cur_id; a.tie = nullptr;
@@ -457,9 +461,12 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
       }
       return FFB_OK;
     }
-    if ((int64_t)h_count * 2 > cur_n && cur_n > 4 * chunk)
-      return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: candidate set does not reduce (%llu of %lld on chunk fronts)",
-                      h_count, (long long)cur_n);
+    if ((int64_t)h_count * 4 > cur_n * 3) {
+      if ((int64_t)h_count > (1 << 20))
+        return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: candidate set does not reduce (%llu of %lld on chunk fronts)",
+                        h_count, (long long)cur_n);
+      stalled = true;
+    }
     cur_e = buf_e[which]; cur_t = buf_t[which]; cur_id = buf_id[which];
     cur_n = (int64_t)h_count;
     which ^= 1;
