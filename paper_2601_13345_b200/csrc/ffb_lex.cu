@@ -138,17 +138,55 @@ FFB_D bool chunk_has(const uint8_t* s, int c0, int c1, unsigned ch) {
 }
 
 // ---- opcode classification (ptx.py:99-136, :64-76) ---------------------------------------------
+// Dot-separated tokens of at most 8 bytes are packed into one u64 and looked up in a 256-slot
+// perfect-hash table held in shared memory (multiplier found offline: no two of the 61 tokens
+// the classifier knows share a slot).
 struct OpcodeInfo {
   uint32_t cls, space, bytes, base, cmp;
 };
+constexpr uint64_t kTokMul = 0x142fcb2e01c7132dull;
+enum { TB_NONE = 0, TB_BAR, TB_BARRIER, TB_LD, TB_LDU, TB_ST, TB_BRA, TB_ADD, TB_SUB, TB_MUL, TB_MAD, TB_FMA, TB_DIV,
+       TB_SIN, TB_COS, TB_EX2, TB_LG2, TB_RCP, TB_RSQRT, TB_SQRT, TB_MOV, TB_SETP, TB_AND, TB_OR, TB_SHL, TB_SHR,
+       TB_CVT, TB_SELP, TB_CVTA, TB_RET, TB_EXIT };
+// token value: [4:0] base code  [7:5] element bytes code (1:1 2:2 3:4 4:8)  [8] float type  [9] int type
+//              [11:10] vector (1:v2 2:v4)  [12] sync  [15:13] space + 1  [16] approx  [19:17] compare
+constexpr uint32_t tv_base(uint32_t b) { return b; }
+constexpr uint32_t tv_type(uint32_t code, bool f, bool i) { return (code << 5) | (f ? 1u << 8 : 0u) | (i ? 1u << 9 : 0u); }
+struct TokDef { uint64_t key; uint32_t val; };
+__constant__ TokDef kTokDefs[] = {
+  {ffb_pk("bar"), TB_BAR}, {ffb_pk("barrier"), TB_BARRIER}, {ffb_pk("ld"), TB_LD}, {ffb_pk("ldu"), TB_LDU},
+  {ffb_pk("st"), TB_ST}, {ffb_pk("bra"), TB_BRA}, {ffb_pk("add"), TB_ADD}, {ffb_pk("sub"), TB_SUB},
+  {ffb_pk("mul"), TB_MUL}, {ffb_pk("mad"), TB_MAD}, {ffb_pk("fma"), TB_FMA}, {ffb_pk("div"), TB_DIV},
+  {ffb_pk("sin"), TB_SIN}, {ffb_pk("cos"), TB_COS}, {ffb_pk("ex2"), TB_EX2}, {ffb_pk("lg2"), TB_LG2},
+  {ffb_pk("rcp"), TB_RCP}, {ffb_pk("rsqrt"), TB_RSQRT}, {ffb_pk("sqrt"), TB_SQRT}, {ffb_pk("mov"), TB_MOV},
+  {ffb_pk("setp"), TB_SETP}, {ffb_pk("and"), TB_AND}, {ffb_pk("or"), TB_OR}, {ffb_pk("shl"), TB_SHL},
+  {ffb_pk("shr"), TB_SHR}, {ffb_pk("cvt"), TB_CVT}, {ffb_pk("selp"), TB_SELP}, {ffb_pk("cvta"), TB_CVTA},
+  {ffb_pk("ret"), TB_RET}, {ffb_pk("exit"), TB_EXIT},
+  {ffb_pk("b8"), tv_type(1, false, false)}, {ffb_pk("s8"), tv_type(1, false, false)}, {ffb_pk("u8"), tv_type(1, false, false)},
+  {ffb_pk("b16"), tv_type(2, false, false)}, {ffb_pk("s16"), tv_type(2, false, false)}, {ffb_pk("u16"), tv_type(2, false, false)},
+  {ffb_pk("f16"), tv_type(2, false, false)}, {ffb_pk("bf16"), tv_type(2, false, false)},
+  {ffb_pk("b32"), tv_type(3, false, false)}, {ffb_pk("s32"), tv_type(3, false, true)}, {ffb_pk("u32"), tv_type(3, false, true)},
+  {ffb_pk("f32"), tv_type(3, true, false)}, {ffb_pk("b64"), tv_type(4, false, false)}, {ffb_pk("s64"), tv_type(4, false, true)},
+  {ffb_pk("u64"), tv_type(4, false, true)}, {ffb_pk("f64"), tv_type(4, true, false)},
+  {ffb_pk("v2"), 1u << 10}, {ffb_pk("v4"), 2u << 10}, {ffb_pk("sync"), 1u << 12},
+  {ffb_pk("global"), (uint32_t)(FFB_SP_GLOBAL + 1) << 13}, {ffb_pk("shared"), (uint32_t)(FFB_SP_SHARED + 1) << 13},
+  {ffb_pk("local"), (uint32_t)(FFB_SP_LOCAL + 1) << 13}, {ffb_pk("param"), (uint32_t)(FFB_SP_PARAM + 1) << 13},
+  {ffb_pk("const"), (uint32_t)(FFB_SP_PARAM + 1) << 13}, {ffb_pk("approx"), 1u << 16},
+  {ffb_pk("lt"), (uint32_t)FFB_CMP_LT << 17}, {ffb_pk("ge"), (uint32_t)FFB_CMP_GE << 17}, {ffb_pk("le"), (uint32_t)FFB_CMP_LE << 17},
+  {ffb_pk("gt"), (uint32_t)FFB_CMP_GT << 17}, {ffb_pk("eq"), (uint32_t)FFB_CMP_EQ << 17}, {ffb_pk("ne"), (uint32_t)FFB_CMP_NE << 17},
+};
+constexpr int kNumTokDefs = sizeof(kTokDefs) / sizeof(kTokDefs[0]);
+struct TokTable { const uint64_t* key; const uint32_t* val; };
 
-FFB_D OpcodeInfo classify_opcode(const uint8_t* s, int o0, int o1) {
+FFB_D uint32_t tok_lookup(const TokTable& tt, uint64_t pk) {
+  const uint32_t i = (uint32_t)((pk * kTokMul) >> 56);
+  return tt.key[i] == pk ? tt.val[i] : 0u;
+}
+
+FFB_D OpcodeInfo classify_opcode(const TokTable& tt, const uint8_t* s, int o0, int o1) {
   uint64_t pk = 0;
   int tl = 0, ti = 0;
-  uint64_t base_pk = 0;
-  bool has_f = false, has_i = false, has_approx = false, last_sync = false;
-  uint32_t elem = 4, vec = 1, space = FFB_SP_NONE, cmp = FFB_CMP_NONE;
-  bool space_set = false;
+  uint32_t base = TB_NONE, elem_code = 0, vec = 0, space = 0, cmp = 0, flags = 0;   // flags: 1 f, 2 i, 4 approx, 8 last-is-sync
   for (int i = o0; i <= o1; ++i) {
     const unsigned c = i < o1 ? s[i] : (unsigned)'.';
     if (c != '.') {
@@ -156,82 +194,59 @@ FFB_D OpcodeInfo classify_opcode(const uint8_t* s, int o0, int o1) {
       ++tl;
       continue;
     }
-    if (tl > 8) pk = ~0ull;
-    last_sync = false;
-    if (ti == 0) base_pk = pk;
-    // tokens valid at any position
-    if (cmp == FFB_CMP_NONE) {
-      switch (pk) {
-        case ffb_pk("lt"): cmp = FFB_CMP_LT; break;
-        case ffb_pk("ge"): cmp = FFB_CMP_GE; break;
-        case ffb_pk("le"): cmp = FFB_CMP_LE; break;
-        case ffb_pk("gt"): cmp = FFB_CMP_GT; break;
-        case ffb_pk("eq"): cmp = FFB_CMP_EQ; break;
-        case ffb_pk("ne"): cmp = FFB_CMP_NE; break;
-        default: break;
-      }
+    const uint32_t v = tl > 8 ? 0u : tok_lookup(tt, pk);
+    flags &= ~8u;
+    if (ti == 0) base = v & 31u;
+    else {
+      const uint32_t ec = (v >> 5) & 7u;
+      if (ec) elem_code = ec;
+      flags |= (v >> 8) & 3u;                       // float / int type seen (ptx.py:116-119)
+      const uint32_t vc = (v >> 10) & 3u;
+      if (vc) vec = vc;
+      if (v & (1u << 12)) flags |= 8u;
+      const uint32_t sp = (v >> 13) & 7u;
+      if (sp && !space) space = sp;                 // first space token wins (ptx.py:131-135)
     }
-    if (pk == ffb_pk("approx")) has_approx = true;
-    if (ti > 0) {
-      switch (pk) {
-        case ffb_pk("b8"): case ffb_pk("s8"): case ffb_pk("u8"): elem = 1; break;
-        case ffb_pk("b16"): case ffb_pk("s16"): case ffb_pk("u16"): case ffb_pk("f16"): case ffb_pk("bf16"): elem = 2; break;
-        case ffb_pk("b32"): elem = 4; break;
-        case ffb_pk("s32"): case ffb_pk("u32"): elem = 4; has_i = true; break;
-        case ffb_pk("f32"): elem = 4; has_f = true; break;
-        case ffb_pk("b64"): elem = 8; break;
-        case ffb_pk("s64"): case ffb_pk("u64"): elem = 8; has_i = true; break;
-        case ffb_pk("f64"): elem = 8; has_f = true; break;
-        case ffb_pk("v2"): vec = 2; break;
-        case ffb_pk("v4"): vec = 4; break;
-        case ffb_pk("sync"): last_sync = true; break;
-        case ffb_pk("global"): if (!space_set) { space = FFB_SP_GLOBAL; space_set = true; } break;
-        case ffb_pk("shared"): if (!space_set) { space = FFB_SP_SHARED; space_set = true; } break;
-        case ffb_pk("local"): if (!space_set) { space = FFB_SP_LOCAL; space_set = true; } break;
-        case ffb_pk("param"): case ffb_pk("const"): if (!space_set) { space = FFB_SP_PARAM; space_set = true; } break;
-        default: break;
-      }
-    }
+    if (v & (1u << 16)) flags |= 4u;
+    if (!cmp) cmp = (v >> 17) & 7u;                 // first compare token, any position (cfg.py:222)
     pk = 0; tl = 0; ++ti;
   }
   OpcodeInfo r;
-  r.bytes = elem * vec;
+  const uint32_t elem = elem_code == 0 ? 4u : (1u << (elem_code - 1));
+  r.bytes = elem * (vec == 0 ? 1u : (vec == 1 ? 2u : 4u));
   r.cmp = cmp;
   r.space = FFB_SP_NONE;
   r.base = FFB_BASE_OTHER;
-  switch (base_pk) {
-    case ffb_pk("mov"): r.base = FFB_BASE_MOV; break;
-    case ffb_pk("cvt"): r.base = FFB_BASE_CVT; break;
-    case ffb_pk("cvta"): r.base = FFB_BASE_CVTA; break;
-    case ffb_pk("add"): r.base = FFB_BASE_ADD; break;
-    case ffb_pk("sub"): r.base = FFB_BASE_SUB; break;
-    case ffb_pk("mul"): r.base = FFB_BASE_MUL; break;
-    case ffb_pk("mad"): r.base = FFB_BASE_MAD; break;
-    case ffb_pk("fma"): r.base = FFB_BASE_FMA; break;
-    case ffb_pk("shl"): r.base = FFB_BASE_SHL; break;
-    case ffb_pk("setp"): r.base = FFB_BASE_SETP; break;
-    case ffb_pk("ret"): r.base = FFB_BASE_RET; break;
-    case ffb_pk("exit"): r.base = FFB_BASE_EXIT; break;
+  switch (base) {
+    case TB_MOV: r.base = FFB_BASE_MOV; break;
+    case TB_CVT: r.base = FFB_BASE_CVT; break;
+    case TB_CVTA: r.base = FFB_BASE_CVTA; break;
+    case TB_ADD: r.base = FFB_BASE_ADD; break;
+    case TB_SUB: r.base = FFB_BASE_SUB; break;
+    case TB_MUL: r.base = FFB_BASE_MUL; break;
+    case TB_MAD: r.base = FFB_BASE_MAD; break;
+    case TB_FMA: r.base = FFB_BASE_FMA; break;
+    case TB_SHL: r.base = FFB_BASE_SHL; break;
+    case TB_SETP: r.base = FFB_BASE_SETP; break;
+    case TB_RET: r.base = FFB_BASE_RET; break;
+    case TB_EXIT: r.base = FFB_BASE_EXIT; break;
     default: break;
   }
   // decision order of ptx.py:108-128
-  if (base_pk == ffb_pk("bar") || base_pk == ffb_pk("barrier") || last_sync) { r.cls = FFB_CLS_SYNC; return r; }
-  if (base_pk == ffb_pk("ld") || base_pk == ffb_pk("ldu")) { r.cls = FFB_CLS_MEMLOAD; r.space = space; return r; }
-  if (base_pk == ffb_pk("st")) { r.cls = FFB_CLS_MEMSTORE; r.space = space; return r; }
-  if (base_pk == ffb_pk("bra")) { r.cls = FFB_CLS_BRANCH; return r; }
-  switch (base_pk) {
-    case ffb_pk("add"): case ffb_pk("sub"): case ffb_pk("mul"): case ffb_pk("mad"): case ffb_pk("fma"): case ffb_pk("div"):
-      r.cls = has_f ? FFB_CLS_FP32 : (has_i ? FFB_CLS_INT : FFB_CLS_OTHER); return r;
-    case ffb_pk("sin"): case ffb_pk("cos"): case ffb_pk("ex2"): case ffb_pk("lg2"): case ffb_pk("rcp"): case ffb_pk("rsqrt"):
-      r.cls = FFB_CLS_SFU; return r;
-    case ffb_pk("sqrt"):
-      r.cls = has_approx ? FFB_CLS_SFU : FFB_CLS_OTHER; return r;
-    case ffb_pk("mov"): case ffb_pk("setp"): case ffb_pk("and"): case ffb_pk("or"): case ffb_pk("shl"): case ffb_pk("shr"):
-    case ffb_pk("cvt"): case ffb_pk("selp"):
-      r.cls = FFB_CLS_ALU; return r;
-    default: break;
-  }
-  r.cls = FFB_CLS_OTHER;
+  const uint32_t bit = 1u << base;
+  constexpr uint32_t kArith = (1u << TB_ADD) | (1u << TB_SUB) | (1u << TB_MUL) | (1u << TB_MAD) | (1u << TB_FMA) | (1u << TB_DIV);
+  constexpr uint32_t kSfu = (1u << TB_SIN) | (1u << TB_COS) | (1u << TB_EX2) | (1u << TB_LG2) | (1u << TB_RCP) | (1u << TB_RSQRT);
+  constexpr uint32_t kAlu = (1u << TB_MOV) | (1u << TB_SETP) | (1u << TB_AND) | (1u << TB_OR) | (1u << TB_SHL) | (1u << TB_SHR) |
+                            (1u << TB_CVT) | (1u << TB_SELP);
+  if (base == TB_BAR || base == TB_BARRIER || (flags & 8u)) r.cls = FFB_CLS_SYNC;
+  else if (base == TB_LD || base == TB_LDU) { r.cls = FFB_CLS_MEMLOAD; r.space = space ? space - 1 : FFB_SP_NONE; }
+  else if (base == TB_ST) { r.cls = FFB_CLS_MEMSTORE; r.space = space ? space - 1 : FFB_SP_NONE; }
+  else if (base == TB_BRA) r.cls = FFB_CLS_BRANCH;
+  else if (bit & kArith) r.cls = (flags & 1u) ? FFB_CLS_FP32 : ((flags & 2u) ? FFB_CLS_INT : FFB_CLS_OTHER);
+  else if (bit & kSfu) r.cls = FFB_CLS_SFU;
+  else if (base == TB_SQRT) r.cls = (flags & 4u) ? FFB_CLS_SFU : FFB_CLS_OTHER;
+  else if (bit & kAlu) r.cls = FFB_CLS_ALU;
+  else r.cls = FFB_CLS_OTHER;
   return r;
 }
 
@@ -444,6 +459,7 @@ struct LineSummary {
 struct Emit {
   // where this lane's results go (record mode) and its accumulators
   const LexArgs* a;
+  TokTable tok;          // shared-memory token table
   int64_t seg;            // segment index
   int64_t seg_begin;      // global offset of the segment
   int64_t abase;          // global offset of smem index 0
@@ -492,7 +508,7 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
   const int o0 = i;
   int o1 = o0;
   while (o1 < e && !ffb_is_ws(s[o1])) ++o1;
-  const OpcodeInfo oc = classify_opcode(s, o0, o1);
+  const OpcodeInfo oc = classify_opcode(em.tok, s, o0, o1);
   em.cnt[oc.cls] += 1;
   if (kMode < 2) { em.ins_at += 1; return; }
 
@@ -677,10 +693,17 @@ lex_corpus_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
   __shared__ uint8_t s_cls[256];
+  __shared__ uint64_t s_tok_key[256];
+  __shared__ uint32_t s_tok_val[256];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* s = smem_raw + (size_t)wid * kWarpSmem;
   uint16_t* nl = reinterpret_cast<uint16_t*>(s + kTile + kPad);
-  for (int c = threadIdx.x; c < 256; c += kWarps * 32) s_cls[c] = char_class((unsigned)c);
+  for (int c = threadIdx.x; c < 256; c += kWarps * 32) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kNumTokDefs; c += kWarps * 32) {
+    const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
+    s_tok_key[slot] = kTokDefs[c].key; s_tok_val[slot] = kTokDefs[c].val;
+  }
   __syncthreads();
 
   for (;;) {
@@ -706,6 +729,7 @@ lex_corpus_kernel(LexArgs a) {
 
     Emit em;
     em.a = &a; em.seg = seg; em.seg_begin = seg_begin; em.abase = 0; em.line = 0;
+    em.tok.key = s_tok_key; em.tok.val = s_tok_val;
     em.ins_at = kRecords ? a.ins_base[seg] : 0;
     em.lab_at = kRecords ? a.lab_base[seg] : 0;
     em.dcl_at = 0;

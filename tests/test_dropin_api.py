@@ -1,0 +1,163 @@
+"""The drop-in entry points (paper_2601_13345_b200.api) against reference outputs recorded in
+tests/golden/ — the same checks the reference's own suite makes, through the
+kernels.  Runs on the SIMT-emulated build (CPU suite) and on the GPU (-m gpu)."""
+from __future__ import annotations
+
+import json
+import math
+from pathlib import Path
+
+import pytest
+
+from paper_2601_13345_b200 import api, specs
+from paper_2601_13345_b200 import errors as E
+
+G = Path(__file__).parent / "golden"
+PARSE = json.loads((G / "ref_parse.json").read_text())
+MODEL = json.loads((G / "ref_model.json").read_text())
+FIXT = json.loads((G / "ref_fixtures.json").read_text())
+hx = float.hex
+
+
+def _names(backend):
+    names = sorted(PARSE)
+    if backend == "emul":          # the emulated kernels are slow: a representative subset
+        names = [n for n in names if n.startswith(("fixture_", "edge_")) or n in ("synth_0", "nvcc_sm_70_tiled_matmul")]
+    return names
+
+
+def test_parse_cfg_trips_alignment(backend):
+    for name in _names(backend):
+        case = PARSE[name]
+        exp = case["expect"]
+        if "error" in exp:
+            with pytest.raises(getattr(E, exp["error"])):
+                api.parse_ptx(case["source"], case["kernel"])
+            continue
+        m = api.parse_ptx(case["source"], case["kernel"])
+        assert m.kernel_name == exp["kernel_name"] and [list(p) for p in m.parameters] == exp["parameters"], name
+        assert m.registers_declared == exp["registers_declared"] and m.static_shared_bytes == exp["static_shared_bytes"]
+        assert [[i.opcode, i.opcode_class, i.state_space, list(i.operands), i.predicate, i.source_line]
+                for i in m.instructions] == exp["instructions"], name
+        assert m.labels == exp["labels"]
+        cfg0 = api.build_cfg(m)
+        assert [list(b) for b in cfg0.blocks] == exp["blocks"] and [list(e) for e in cfg0.edges] == exp["edges"]
+        assert all(l.trip is None for l in cfg0.loops)
+        for key in ("expect", "expect_trip5"):
+            if key not in case:
+                continue
+            ex = case[key]
+            cfg = api.estimate_trip_counts(cfg0, m, default_trip=ex["default_trip"])
+            assert [[l.header, sorted(l.body), l.header_label, hx(l.trip)] for l in cfg.loops] == ex["loops"], name
+            assert hx(api.analyze_memory_alignment(m, cfg)) == ex["aligned_fraction"], name
+            n_mem, mem_bytes, by_unit, n_sync = api.dynamic_instruction_counts(m, cfg)
+            got = {"n_mem": n_mem, "mem_bytes": mem_bytes, "n_sync": n_sync, **by_unit}
+            assert {k: hx(v) for k, v in got.items()} == ex["dynamic"], name
+
+
+def test_annotations(backend):
+    src = FIXT["sources"]["counted_loop"]
+    m = api.parse_ptx(src)
+    cfg = api.build_cfg(m)
+    label = cfg.loops[0].header_label
+    assert api.estimate_trip_counts(cfg, m, annotations={label: 10.0}).loops[0].trip == 10.0
+    assert api.estimate_trip_counts(cfg, m, annotations={label: 0.25}).loops[0].trip == 1.0
+    with pytest.raises(E.AnnotationForUnknownLoop):
+        api.estimate_trip_counts(cfg, m, annotations={"nope": 3.0})
+
+
+def _spec(name):
+    if name == "default":
+        return specs.default_architecture(), specs.default_calibration()
+    return specs.architecture_from_dict(MODEL["alt_spec"]["arch"]), specs.calibration_from_dict(MODEL["alt_spec"]["calibration"])
+
+
+def test_explore_pipeline(backend):
+    cases = MODEL["cases"] if backend == "gpu" else MODEL["cases"][:3]
+    for case in cases:
+        a, p = _spec(case["spec"])
+        m = api.parse_ptx(FIXT["sources"][case["fixture"]])
+        cfg = api.estimate_trip_counts(api.build_cfg(m), m)
+        sd, gx, gy, gz = case["resources"]
+        res = api.InputResources(sd, gx, gy, gz)
+        cfgs = api.generate_valid_configs(a, res, case["dims"], case["caps"])
+        assert [[c.block_x, c.block_y, c.p_cap] for c in cfgs] == case["configs"]
+        preds = api.evaluate_configs(m, cfg, a, p, res, cfgs, jobs=4)
+        assert [[hx(q.time.t_exec), hx(q.power.p_dyn), hx(q.e_pred), q.power.cap_limited] for q in preds] == case["pred"]
+        for q, d in zip(preds, case["detail"]):
+            got = [q.time.t_mem, q.time.t_comp, q.time.t_sync, q.time.mwp, q.time.cwp, q.time.bw_eff, q.power.p_units,
+                   q.power.p_shape, q.power.p_mem, q.power.p_sm, q.power.f_adj, q.power.ci]
+            assert [hx(x) for x in got] + [q.power.active_sms] == d
+            assert q.e_pred == q.time.t_exec * (q.power.p_dyn + a.p_static) + p.e_overhead     # explorer.py:107
+        for rho, exp in case["fronts"].items():
+            ps = api.pareto_explore(m, cfg, a, p, res, case["dims"], case["caps"], rho=float(rho))
+            assert [[e.config.block_x, e.config.block_y, e.config.p_cap] for e in ps.entries] == exp["entries"]
+            assert hx(ps.t_peak) == exp["t_peak"] and ps.rho == float(rho)
+        f = api.extract_features(m, cfg, cfgs[0], res, a)
+        one = api.predict_energy(f, a, p, cfgs[0], res)
+        assert one == preds[[c for c in sorted(cfgs, key=lambda c: (c.threads, c.block_x, c.block_y, c.p_cap))].index(cfgs[0])]
+
+
+def test_pareto_front_clouds(backend):
+    clouds = json.loads((G / "ref_pareto.json").read_text())
+    for c in clouds[: (40 if backend == "gpu" else 6)]:
+        preds = []
+        for e, t, (bx, by, cap) in zip(c["e"], c["t"], c["cfg"]):
+            tb = api.TimeBreakdown(1.0, 1.0, 1.0, 0.0, 0.0, 0.0, float.fromhex(t))
+            pb = api.PowerBreakdown(0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1, False)
+            preds.append(api.Prediction(api.LaunchConfig(bx, by, cap), tb, pb, float.fromhex(e)))
+        front = api.pareto_front(preds)
+        assert [preds.index(q) for q in front] == c["front"] or [id(q) for q in front] == [id(preds[i]) for i in c["front"]]
+        ps = api.pareto_front_bruteforce(preds)
+        assert [id(q) for q in ps.entries] == [id(preds[i]) for i in c["front"]] and hx(ps.t_peak) == c["t_peak"]
+    with pytest.raises(E.NoFeasibleConfig):
+        api.pareto_front_bruteforce([])
+    assert api.pareto_front([]) == []
+
+
+def test_model_helpers_known_answers(backend):
+    k = MODEL["kats"]
+    assert hx(api.shape_power(10.0, 0.1, 2, 32, 1.0)) == k["shape_power(10,0.1,2,32,1)"]
+    assert api.shape_power(10.0, 0.1, 16, 16, 1.0) == 10.0 and api.shape_power(10.0, 0.1, 2, 32, math.inf) == 10.0
+    assert hx(api.sm_concurrency_power(16, 2.0, 0.8, 30.0)) == k["sm_concurrency_power(16,2,0.8,30)"]
+    assert api.sm_concurrency_power(0, 2.0, 0.8, 30.0) == 30.0 and api.sm_concurrency_power(1, 2.0, 0.8, 30.0) == 32.0
+    assert hx(api.dvfs_frequency(1.0, 125.0, 250.0, 3)) == k["dvfs_frequency(1,125,250,3)"]
+    assert hx(api.dvfs_frequency(1.0, 100.0, 250.0, 3)) == k["dvfs_frequency(1,100,250,3)"]
+    assert api.dvfs_frequency(1.5e9, 250.0, 250.0, 3) == 1.5e9
+    assert api.memory_power(20.0, 0.5, 1.0) == 20.0 and api.memory_power(20.0, 0.5, 0.0) == 30.0
+    assert hx(api.memory_power(20.0, 0.25, 0.6)) == k["memory_power(20,0.25,0.6)"]
+    assert hx(api.transient_correction(100.0, 5e-6, 1e-5, 0.833)) == k["transient_correction(100,5e-6,1e-5,0.833)"]
+    assert api.transient_correction(100.0, 2e-5, 1e-5, 0.833) == 100.0
+    assert hx(api.activity_rate(100.0, 8.0, 4.0, 1.0)) == k["activity_rate(100,8,4,1)"]
+    assert api.mwp(400.0, 40.0) == 10.0 and api.mwp(20.0, 40.0) == 1.0
+    assert api.cwp(0.0, 100.0) == 1.0 and api.cwp(300.0, 100.0) == 4.0
+    assert api.compute_intensity(100.0, 0.0) == math.inf and api.compute_intensity(0.0, 100.0) == 0.0
+    assert api.coalescing_efficiency(16, 0.5) == 0.25 and api.coalescing_efficiency(64, 1.0) == 1.0
+    with pytest.raises(E.ZeroDelay):
+        api.mwp(400.0, 0.0)
+    with pytest.raises(E.ZeroComputeCycles):
+        api.cwp(100.0, 0.0)
+    with pytest.raises(E.CapAboveTdp):
+        api.dvfs_frequency(1.0, 300.0, 250.0, 3)
+    with pytest.raises(E.InvalidConfig):
+        api.coalescing_efficiency(0, 1.0)
+
+
+def test_classifier_and_errors(backend):
+    table = json.loads((G / "ref_classify.json").read_text())
+    ops = list(table)[: (len(table) if backend == "gpu" else 12)]
+    for op in ops:
+        assert list(api.classify_opcode(op)) == table[op][:2], op
+    a = specs.default_architecture()
+    with pytest.raises(E.SharedMemOverflow):
+        api.compute_input_resources(100000, 1, 1, 64, 4, a)
+    r = api.compute_input_resources(128, 2, 8, 64, 2, a)
+    assert (r.shared_mem_bytes, r.grid_x, r.grid_y, r.total_blocks) == (2 * (64 + 128), 8, 2, 16)
+    m = api.parse_ptx(FIXT["sources"]["vecadd"])
+    cfg = api.estimate_trip_counts(api.build_cfg(m), m)
+    with pytest.raises(E.InvalidConfig):
+        api.extract_features(m, cfg, api.LaunchConfig(5, 5, 200.0), api.InputResources(0), a)
+    with pytest.raises(ValueError):
+        api.pareto_explore(m, cfg, a, specs.default_calibration(), api.InputResources(0), [32], None, rho=0.0)
+    with pytest.raises(E.NoFeasibleConfig):
+        api.pareto_explore(m, cfg, a, specs.default_calibration(), api.InputResources(0), [3, 5], None)
