@@ -91,6 +91,8 @@ FFB_D unsigned long long warp_sum_u64(unsigned long long v) {
   return v;
 }
 
+FFB_D int next_bit(const uint32_t m[4], int from);
+
 // ---- T1: comment automaton ------------------------------------------------------------------
 FFB_D int cm_step(int st, unsigned c) {
   const bool sl = c == '/', star = c == '*', nl = c == '\n';
@@ -109,8 +111,12 @@ FFB_D int cm_step(int st, unsigned c) {
 
 // Runs the automaton over s[c0,c1) from state `st`; when `blank` is set rewrites comment
 // bytes to ' ' (newlines inside block comments become kNlInBlock).  Returns the exit state.
-FFB_D int cm_run(uint8_t* s, int c0, int c1, int st, bool blank) {
+FFB_D int cm_run(uint8_t* s, int c0, int c1, int st, bool blank, const uint32_t slash[4], int chunk_base) {
   for (int i = c0; i < c1; ++i) {
+    if (st == S_CODE) {                       // nothing happens in code until the next '/'
+      i = chunk_base + next_bit(slash, i - chunk_base);
+      if (i >= c1) break;
+    }
     const unsigned c = s[i];
     const int nx = cm_step(st, c);
     if (blank) {
@@ -131,10 +137,48 @@ FFB_D int cm_run(uint8_t* s, int c0, int c1, int st, bool blank) {
   return st;
 }
 
-FFB_D bool chunk_has(const uint8_t* s, int c0, int c1, unsigned ch) {
-  for (int i = c0; i < c1; ++i)
-    if (s[i] == ch) return true;
-  return false;
+// 4-bit mask (bit i <-> byte i) of the bytes of w equal to the replicated pattern
+FFB_D uint32_t eq_nibble(uint32_t w, uint32_t pattern) {
+  const uint32_t m = __vcmpeq4(w, pattern) & 0x08040201u;
+  return (m * 0x01010101u) >> 24;
+}
+// 128-bit position masks of a lane's aligned 128-byte chunk: bytes equal to pat_a or pat_b
+// (mask_ab) and bytes equal to pat_b alone (mask_b).  Bits outside [lo_bit, hi_bit) are cleared.
+FFB_D void chunk_masks(const uint8_t* chunk, uint32_t pat_a, uint32_t pat_b, int lo_bit, int hi_bit,
+                       uint32_t mask_ab[4], uint32_t mask_b[4]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const uint4 q = *reinterpret_cast<const uint4*>(chunk + v * 16);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t ab = 0, b = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t nb = eq_nibble(w[j], pat_b);
+      ab |= (eq_nibble(w[j], pat_a) | nb) << (4 * j);
+      b |= nb << (4 * j);
+    }
+    // v covers bytes [16v, 16v+16): halves of the 32-bit mask words
+    if (v & 1) { mask_ab[v >> 1] |= ab << 16; mask_b[v >> 1] |= b << 16; }
+    else { mask_ab[v >> 1] = ab; mask_b[v >> 1] = b; }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int lo = lo_bit - 32 * k, hi = hi_bit - 32 * k;
+    uint32_t keep = 0xffffffffu;
+    if (lo > 0) keep &= lo >= 32 ? 0u : (0xffffffffu << lo);
+    if (hi < 32) keep &= hi <= 0 ? 0u : (0xffffffffu >> (32 - hi));
+    mask_ab[k] &= keep; mask_b[k] &= keep;
+  }
+}
+FFB_D int next_bit(const uint32_t m[4], int from) {       // first set bit at position >= from, or 128
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (from >= 32 * (k + 1)) continue;
+    const int sh = from > 32 * k ? from - 32 * k : 0;
+    const uint32_t x = m[k] & (0xffffffffu << sh);
+    if (x) return 32 * k + __ffs((int)x) - 1;
+  }
+  return 128;
 }
 
 // ---- opcode classification (ptx.py:99-136, :64-76) ---------------------------------------------
@@ -757,8 +801,11 @@ lex_corpus_kernel(LexArgs a) {
       em.abase = abase;
 
       // ================= T1: comments =================
-      const int c0 = max(lane * kLaneBytes, lo), c1 = min(lane * kLaneBytes + kLaneBytes, hi);
-      const bool has_slash = chunk_has(s, c0, c1, '/');
+      const int chunk_base = lane * kLaneBytes;
+      const int c0 = max(chunk_base, lo), c1 = min(chunk_base + kLaneBytes, hi);
+      uint32_t slash[4], unused4[4];
+      chunk_masks(s + chunk_base, 0x2f2f2f2fu, 0x2f2f2f2fu, c0 - chunk_base, c1 - chunk_base, slash, unused4);
+      const bool has_slash = (slash[0] | slash[1] | slash[2] | slash[3]) != 0;
       int st_in = S_CODE, st_out = S_CODE;
       {
         bool need = true;
@@ -766,7 +813,7 @@ lex_corpus_kernel(LexArgs a) {
           if (need) {
             if (c0 >= c1) st_out = st_in;
             else if (!has_slash && st_in == S_CODE) st_out = S_CODE;
-            else st_out = cm_run(s, c0, c1, st_in, false);
+            else st_out = cm_run(s, c0, c1, st_in, false, slash, chunk_base);
             need = false;
           }
           int left = __shfl_up_sync(kFull, st_out, 1);
@@ -778,20 +825,26 @@ lex_corpus_kernel(LexArgs a) {
       }
       const bool dirty = (has_slash || st_in != S_CODE) && c0 < c1;
       if (__any_sync(kFull, dirty)) {
-        if (dirty) cm_run(s, c0, c1, st_in, true);
+        if (dirty) cm_run(s, c0, c1, st_in, true, slash, chunk_base);
         __syncwarp();
       }
 
       // ================= T2: line table =================
-      int my_nl = 0;
-      for (int i = c0; i < c1; ++i) my_nl += (s[i] == '\n' || s[i] == kNlInBlock) ? 1 : 0;
+      uint32_t nlm[4], nlb[4];
+      chunk_masks(s + chunk_base, 0x0a0a0a0au, 0x8a8a8a8au, c0 - chunk_base, c1 - chunk_base, nlm, nlb);
+      const int my_nl = __popc(nlm[0]) + __popc(nlm[1]) + __popc(nlm[2]) + __popc(nlm[3]);
       int total_nl = 0;
       int at = warp_excl_sum(my_nl, &total_nl);
-      for (int i = c0; i < c1; ++i) {
-        const unsigned c = s[i];
-        if (c == '\n' || c == kNlInBlock) {
-          if (at < kMaxLines) nl[at] = (uint16_t)(i | (c == kNlInBlock ? 0x8000 : 0));
-          if (c == kNlInBlock) s[i] = '\n';
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t m = nlm[k];
+        while (m) {
+          const int bit = __ffs((int)m) - 1;
+          m &= m - 1;
+          const int i = chunk_base + 32 * k + bit;
+          const bool in_block = (nlb[k] >> bit) & 1u;
+          if (at < kMaxLines) nl[at] = (uint16_t)(i | (in_block ? 0x8000 : 0));
+          if (in_block) s[i] = '\n';
           ++at;
         }
       }

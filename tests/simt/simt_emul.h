@@ -121,6 +121,11 @@ inline unsigned __brev(unsigned v) {
 }
 inline long long __double_as_longlong(double d) { long long r; memcpy(&r, &d, 8); return r; }
 inline double __longlong_as_double(long long v) { double r; memcpy(&r, &v, 8); return r; }
+inline unsigned __vcmpeq4(unsigned a, unsigned b) {
+  unsigned r = 0;
+  for (int i = 0; i < 4; ++i) if (((a >> (8 * i)) & 0xffu) == ((b >> (8 * i)) & 0xffu)) r |= 0xffu << (8 * i);
+  return r;
+}
 inline unsigned __byte_perm(unsigned a, unsigned b, unsigned s) {
   unsigned long long v = ((unsigned long long)b << 32) | a; unsigned r = 0;
   for (int i = 0; i < 4; ++i) { unsigned sel = (s >> (4 * i)) & 7u; r |= (unsigned)((v >> (8 * sel)) & 0xffu) << (8 * i); }
