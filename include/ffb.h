@@ -220,10 +220,16 @@ typedef struct {
   const int64_t* d_lab_base;  /* [K] */
   void* d_ins;                /* FfbInsRecC[sum n_instr]                                        */
   void* d_labels;             /* FfbLabelRecC[sum n_labels]                                     */
+  uint32_t* d_meta;           /* optional [sum n_instr]: copy of FfbInsRecC.meta, 4 B per instruction
+                                 (the structural passes of K1b stream this instead of the records) */
   FfbSpanRec* d_spans;        /* optional, parallel to d_ins                                    */
   FfbDeclRec* d_decls;        /* optional, [K, FFB_MAX_DECLS]                                   */
 } FfbLexDesc;
 int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream);
+/* classify_opcode (ptx.py:99) and Instruction.access_bytes (ptx.py:64) for n opcode strings:
+ * string i is d_text[d_off[i] : d_off[i+1]); d_out[n,3] = {class, state space, access bytes}. */
+int32_t ffb_classify_opcodes(FfbContext* ctx, const uint8_t* d_text, const int64_t* d_off, int64_t n,
+                             uint32_t* d_out, void* stream);
 
 /* ---- K1b: control flow, trip counts, affine alignment, dynamic counts ------------------
  * Stands in for ptx.py:277-284 (branch targets), cfg.py:57-279 (build_cfg,
@@ -252,6 +258,7 @@ typedef struct {
   const int64_t* d_lab_base;      /* [K] */
   const void* d_ins;              /* FfbInsRecC[n_ins_total]                                   */
   const void* d_labels;           /* FfbLabelRecC[n_lab_total]                                 */
+  const uint32_t* d_meta;         /* optional [n_ins_total] from ffb_lex_corpus (faster when given) */
   int64_t n_ins_total, n_lab_total;
   const int32_t* d_order;         /* optional [K] processing order                             */
   double default_trip;            /* cfg.py:157 (reference default 32.0)                       */

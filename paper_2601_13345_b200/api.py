@@ -136,14 +136,25 @@ def parse_ptx(source: str, kernel_name: str | None = None) -> PtxModule:
                      instructions=tuple(instructions), labels=labels, _dev=handle)
 
 
+def classify_opcodes(opcodes: list[str]) -> list[tuple[str, str, int]]:
+    """Batch form of ptx.py:99 + :64: (class, state space, access bytes) per opcode string."""
+    if not opcodes:
+        return []
+    rt = native.get_runtime()
+    blobs = [o.encode("utf-8") for o in opcodes]
+    offs = np.cumsum([0] + [len(b) for b in blobs]).astype(np.int64)
+    text = rt.to_device(torch.frombuffer(bytearray(b"".join(blobs) + b"\0" * 16), dtype=torch.uint8))
+    d_off = rt.to_device(torch.from_numpy(offs))
+    out = rt.empty((len(opcodes), 3), torch.int32)
+    rc = rt.lib.ffb_classify_opcodes(rt.ctx, native.ptr(text), native.ptr(d_off), len(opcodes), native.ptr(out), rt.stream())
+    rt.check(rc, "ffb_classify_opcodes")
+    return [(OPCODE_CLASSES[c], STATE_SPACES[s], int(b)) for c, s, b in out.cpu().tolist()]
+
+
 def classify_opcode(opcode: str) -> tuple[str, str]:
-    """ptx.py:99 — classification by the device classifier (one-statement kernel)."""
-    if not opcode or any(ch.isspace() for ch in opcode) or ";" in opcode:
-        raise ValueError(f"not a single opcode token: {opcode!r}")
-    tail = "" if opcode.split(".")[0] != "bra" else " L0"
-    mod = parse_ptx(f".entry k()\n{{\nL0: {opcode}{tail};\n}}\n")
-    ins = mod.instructions[0]
-    return ins.opcode_class, ins.state_space
+    """ptx.py:99."""
+    cls, space, _ = classify_opcodes([opcode])[0]
+    return cls, space
 
 
 def _handle_of(module: PtxModule) -> _KernelHandle:

@@ -35,7 +35,8 @@ class LexDesc(C.Structure):
         ("d_text", C.c_void_p), ("n_bytes", C.c_int64), ("d_seg_off", C.c_void_p), ("n_segs", C.c_int64),
         ("d_order", C.c_void_p), ("h_kernel_name", C.c_char_p), ("kernel_name_len", C.c_int32),
         ("d_hist", C.c_void_p), ("d_info", C.c_void_p), ("d_ins_base", C.c_void_p), ("d_lab_base", C.c_void_p),
-        ("d_ins", C.c_void_p), ("d_labels", C.c_void_p), ("d_spans", C.c_void_p), ("d_decls", C.c_void_p),
+        ("d_ins", C.c_void_p), ("d_labels", C.c_void_p), ("d_meta", C.c_void_p), ("d_spans", C.c_void_p),
+        ("d_decls", C.c_void_p),
     ]
 
 
@@ -84,6 +85,7 @@ class LexResult:
     lab_base: torch.Tensor | None = None
     ins: torch.Tensor | None = None      # uint8 [N, 64]
     labels: torch.Tensor | None = None   # uint8 [L, 16]
+    meta: torch.Tensor | None = None     # int32 [N] compact meta words
     spans: torch.Tensor | None = None    # uint8 [N, 128]
     decls: torch.Tensor | None = None    # uint8 [K, 32, 16]
     n_ins: int = 0
@@ -97,14 +99,14 @@ class LexResult:
 
 
 def _call_lex(rt, corp: Corpus, hist, info, *, kernel_name: bytes | None = None, ins_base=None, lab_base=None,
-              ins=None, labels=None, spans=None, decls=None):
+              ins=None, labels=None, meta=None, spans=None, decls=None):
     d = LexDesc(
         d_text=native.ptr(corp.text), n_bytes=corp.padded_bytes, d_seg_off=native.ptr(corp.seg_off),
         n_segs=corp.n_segs, d_order=native.ptr(corp.order),
         h_kernel_name=kernel_name, kernel_name_len=len(kernel_name) if kernel_name else 0,
         d_hist=native.ptr(hist), d_info=native.ptr(info), d_ins_base=native.ptr(ins_base),
         d_lab_base=native.ptr(lab_base), d_ins=native.ptr(ins), d_labels=native.ptr(labels),
-        d_spans=native.ptr(spans), d_decls=native.ptr(decls))
+        d_meta=native.ptr(meta), d_spans=native.ptr(spans), d_decls=native.ptr(decls))
     rc = rt.lib.ffb_lex_corpus(rt.ctx, C.byref(d), rt.stream())
     rt.check(rc, "ffb_lex_corpus")
 
@@ -135,10 +137,11 @@ def lex_records(corp: Corpus, *, kernel_name: str | None = None, spans: bool = F
     res.n_ins, res.n_lab = (int(inc_i[-1]), int(inc_l[-1])) if K else (0, 0)
     res.ins = rt.empty((max(res.n_ins, 1), 64), torch.uint8)
     res.labels = rt.empty((max(res.n_lab, 1), 16), torch.uint8)
+    res.meta = rt.empty((max(res.n_ins, 1),), torch.int32)
     res.spans = torch.zeros((max(res.n_ins, 1), 128), dtype=torch.uint8, device=rt.device) if spans else None
     res.decls = torch.zeros((K, MAX_DECLS, 16), dtype=torch.uint8, device=rt.device) if decls else None
     _call_lex(rt, corp, res.hist, res.info, kernel_name=name, ins_base=res.ins_base, lab_base=res.lab_base,
-              ins=res.ins, labels=res.labels, spans=res.spans, decls=res.decls)
+              ins=res.ins, labels=res.labels, meta=res.meta, spans=res.spans, decls=res.decls)
     return res
 
 
@@ -156,7 +159,8 @@ assert LOOP_DTYPE.itemsize == 32
 class FlowDesc(C.Structure):
     _fields_ = [
         ("n_segs", C.c_int64), ("d_info", C.c_void_p), ("d_ins_base", C.c_void_p), ("d_lab_base", C.c_void_p),
-        ("d_ins", C.c_void_p), ("d_labels", C.c_void_p), ("n_ins_total", C.c_int64), ("n_lab_total", C.c_int64),
+        ("d_ins", C.c_void_p), ("d_labels", C.c_void_p), ("d_meta", C.c_void_p), ("n_ins_total", C.c_int64),
+        ("n_lab_total", C.c_int64),
         ("d_order", C.c_void_p), ("default_trip", C.c_double), ("h_ann_hash", C.c_void_p),
         ("h_ann_trip", C.c_void_p), ("n_ann", C.c_int32), ("d_ann_hit", C.c_void_p), ("d_feat", C.c_void_p),
         ("d_status", C.c_void_p), ("d_flow", C.c_void_p), ("d_block_start", C.c_void_p), ("d_edges", C.c_void_p),
@@ -212,7 +216,8 @@ def kernel_features(corp: Corpus, lex: LexResult, *, default_trip: float = 32.0,
             res.loop_body = torch.zeros(max(1, min((lex.n_ins + 1) ** 2, 1 << 26)), dtype=torch.uint8, device=rt.device)
     d = FlowDesc(
         n_segs=K, d_info=native.ptr(lex.info), d_ins_base=native.ptr(lex.ins_base), d_lab_base=native.ptr(lex.lab_base),
-        d_ins=native.ptr(lex.ins), d_labels=native.ptr(lex.labels), n_ins_total=lex.n_ins, n_lab_total=lex.n_lab,
+        d_ins=native.ptr(lex.ins), d_labels=native.ptr(lex.labels), d_meta=native.ptr(lex.meta), n_ins_total=lex.n_ins,
+        n_lab_total=lex.n_lab,
         d_order=native.ptr(corp.order), default_trip=float(default_trip),
         h_ann_hash=ann_hash.ctypes.data if n_ann else None, h_ann_trip=ann_trip.ctypes.data if n_ann else None,
         n_ann=n_ann, d_ann_hit=native.ptr(res.ann_hit), d_feat=native.ptr(feat), d_status=native.ptr(status),
@@ -288,7 +293,7 @@ class BenchLexState:
         torch.sub(torch.cumsum(n_ins, dim=0), n_ins, out=lex.ins_base)
         torch.sub(torch.cumsum(n_lab, dim=0), n_lab, out=lex.lab_base)
         _call_lex(rt, corp, lex.hist, lex.info, ins_base=lex.ins_base, lab_base=lex.lab_base, ins=lex.ins,
-                  labels=lex.labels)                                      # K1 records
+                  labels=lex.labels, meta=lex.meta)                                      # K1 records
         kernel_features(corp, lex, out_feat=self.feat, rt=rt)             # K1b
         return self.feat
 

@@ -22,6 +22,12 @@
 
 #include <math.h>
 
+#ifdef FFB_SIMT_EMUL
+#define FFB_PREFETCH(p) ((void)(p))
+#else
+#define FFB_PREFETCH(p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p))
+#endif
+
 namespace {
 
 constexpr int kFlowThreads = 64;
@@ -36,6 +42,7 @@ struct FlowArgs {
   const int64_t* lab_base;
   const FfbInsRec* ins;
   const FfbLabelRec* labels;
+  const uint32_t* meta_arr;     // optional compact meta words
   const int32_t* order;
   double default_trip;
   const uint64_t* ann_hash;     // device copies
@@ -197,6 +204,8 @@ flow_kernel(FlowArgs a) {
   const int64_t ib = a.ins_base[k], lb = a.lab_base[k];
   const FfbInsRec* ins = a.ins + ib;
   const FfbLabelRec* lab = a.labels + lb;
+  const uint32_t* cm = a.meta_arr ? a.meta_arr + ib : nullptr;        // compact meta stream
+#define FFB_META(i) (cm ? cm[i] : ins[i].meta)
   const int64_t o1 = ib + 2 * k;                   // offset into the [N + 2K] arrays
   uint32_t* block_of = a.block_of + ib;
   uint32_t* block_start = a.block_start + o1;
@@ -228,7 +237,7 @@ flow_kernel(FlowArgs a) {
     if (lt.last[s] == i && lab[i].index < n) block_of[lab[i].index] = 1;     // effective definition only
   }
   for (uint32_t i = 0; i + 1 < n; ++i) {
-    const uint32_t m = ins[i].meta;
+    const uint32_t m = FFB_META(i);
     const uint32_t base = ffb_meta_base(m);
     if (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT) block_of[i + 1] = 1;
   }
@@ -243,7 +252,7 @@ flow_kernel(FlowArgs a) {
   for (uint32_t b = 0; b < nb; ++b) { succ0[b] = -1; succ1[b] = -1; pred_ptr[b] = 0; }
   pred_ptr[nb] = 0;
   for (uint32_t i = 0; i < n && status == FFB_OK; ++i) {
-    const uint32_t m = ins[i].meta;
+    const uint32_t m = FFB_META(i);
     if (ffb_meta_cls(m) != FFB_CLS_BRANCH) continue;
     const uint64_t tgt = ins[i].aux;
     const uint32_t s = tgt ? lt.find(ffb_op_hash(tgt)) : lt.cap;
@@ -252,7 +261,7 @@ flow_kernel(FlowArgs a) {
   if (status != FFB_OK) { a.status[k] = status; if (a.flow) a.flow[k] = fi; return; }
   for (uint32_t b = 0; b < nb; ++b) {
     const FfbInsRec& last = ins[block_start[b + 1] - 1];
-    const uint32_t m = last.meta;
+    const uint32_t m = FFB_META(block_start[b + 1] - 1);
     const uint32_t base = ffb_meta_base(m);
     if (ffb_meta_cls(m) == FFB_CLS_BRANCH) {
       const uint32_t s = lt.find(ffb_op_hash(last.aux));
@@ -359,7 +368,7 @@ flow_kernel(FlowArgs a) {
       for (uint32_t b = 0; b < nb; ++b) {
         if (mark[b] != stamp) continue;
         for (uint32_t i = block_start[b]; i < block_start[b + 1]; ++i) {
-          const uint32_t m = ins[i].meta;
+          const uint32_t m = FFB_META(i);
           if (ffb_meta_cls(m) == FFB_CLS_BRANCH && ffb_meta_has_pred(m)) {
             const uint32_t s = lt.find(ffb_op_hash(ins[i].aux));
             if (lab[lt.last[s]].index == h0) latch = i;
@@ -373,7 +382,7 @@ flow_kernel(FlowArgs a) {
         for (uint32_t b = 0; b < nb; ++b) {
           if (mark[b] != stamp) continue;
           for (uint32_t i = block_start[b]; i < block_start[b + 1]; ++i) {
-            const uint32_t m = ins[i].meta;
+            const uint32_t m = FFB_META(i);
             if (ffb_meta_base(m) == FFB_BASE_SETP && ffb_meta_nops(m) >= 1 && ffb_op_kind(ins[i].op[0]) != FFB_OPK_INT &&
                 ffb_op_hash(ins[i].op[0]) == preg) cmp_i = i;
           }
@@ -401,7 +410,7 @@ flow_kernel(FlowArgs a) {
         for (uint32_t b = 0; b < nb && ok; ++b) {
           if (mark[b] != stamp) continue;
           for (uint32_t i = block_start[b]; i < block_start[b + 1] && ok; ++i) {
-            const uint32_t m = ins[i].meta;
+            const uint32_t m = FFB_META(i);
             const uint32_t base = ffb_meta_base(m);
             if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && ffb_meta_nops(m) == 3 &&
                 starts_with_percent(ins[i].op[0]) && ffb_op_hash(ins[i].op[0]) == ch &&
@@ -422,8 +431,8 @@ flow_kernel(FlowArgs a) {
         const uint64_t ch = ffb_op_hash(counter);
         // the LAST write before the header decides (cfg.py:246-254), so walk backwards and stop
         for (int64_t i = (int64_t)h0 - 1; i >= 0; --i) {
-          const uint32_t m = ins[i].meta;
-          if (ffb_meta_nops(m) == 0) continue;
+          const uint32_t m = FFB_META(i);
+          if (ffb_meta_nops(m) == 0 || !ffb_meta_dst_reg(m)) continue;      // the counter starts with '%'
           const uint64_t d0 = ins[i].op[0];
           if (!starts_with_percent(d0) || ffb_op_hash(d0) != ch) continue;
           if (ffb_meta_base(m) == FFB_BASE_MOV && ffb_meta_nops(m) == 2) {
@@ -470,6 +479,7 @@ flow_kernel(FlowArgs a) {
   double n_mem = 0.0, mem_bytes = 0.0, u_fp = 0.0, u_int = 0.0, u_sfu = 0.0, u_alu = 0.0, n_sync = 0.0;
   double al_hit = 0.0, al_tot = 0.0;
   for (uint32_t i = 0; i < n; ++i) {
+    if (i + 6 < n) FFB_PREFETCH(&ins[i + 6]);
     const FfbInsRec r = ins[i];
     const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m), base = ffb_meta_base(m);
     const double wgt = weight[block_of[i]];
@@ -573,6 +583,7 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   FlowArgs a = {};
   a.n_segs = K; a.info = d->d_info; a.ins_base = d->d_ins_base; a.lab_base = d->d_lab_base;
   a.ins = (const FfbInsRec*)d->d_ins; a.labels = (const FfbLabelRec*)d->d_labels; a.order = d->d_order;
+  a.meta_arr = d->d_meta;
   a.default_trip = d->default_trip;
   a.n_ann = d->n_ann > 0 ? d->n_ann : 0; a.ann_hit = d->d_ann_hit;
   a.feat = d->d_feat; a.status = d->d_status; a.flow = d->d_flow;

@@ -64,6 +64,7 @@ struct LexArgs {
   const int64_t* lab_base;
   FfbInsRec* ins;
   FfbLabelRec* labels;
+  uint32_t* meta;             // optional compact copy of the meta words
   FfbSpanRec* spans;          // optional, parallel to ins
   FfbDeclRec* decls;          // optional, [K, FFB_MAX_DECLS]
 };
@@ -608,6 +609,7 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
              ((neg ? 1u : 0u) << 19) | ((uint32_t)(count > 7 ? 7 : count) << 20) | (oc.cmp << 23) | (addr_kind << 26) |
              ((dst_reg ? 1u : 0u) << 28) | ((extra_reg ? 1u : 0u) << 29);
   em.a->ins[em.ins_at] = rec;
+  if (em.a->meta) em.a->meta[em.ins_at] = rec.meta;
   em.ins_at += 1;
 }
 
@@ -1101,6 +1103,38 @@ lex_corpus_kernel(LexArgs a) {
   }
 }
 
+// Batch classifier: one thread per opcode string (ptx.py:99-136 and :64-76 as pure functions).
+__global__ void __launch_bounds__(256)
+classify_opcodes_kernel(const uint8_t* text, const int64_t* off, int64_t n, uint32_t* out) {
+  __shared__ uint64_t s_tok_key[256];
+  __shared__ uint32_t s_tok_val[256];
+  s_tok_key[threadIdx.x] = ~0ull; s_tok_val[threadIdx.x] = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < kNumTokDefs; c += 256) {
+    const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
+    s_tok_key[slot] = kTokDefs[c].key; s_tok_val[slot] = kTokDefs[c].val;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= n) return;
+  TokTable tt; tt.key = s_tok_key; tt.val = s_tok_val;
+  const int64_t b = off[i], e = off[i + 1];
+  const OpcodeInfo oc = classify_opcode(tt, text + b, 0, (int)(e - b));
+  out[3 * i] = oc.cls; out[3 * i + 1] = oc.space; out[3 * i + 2] = oc.bytes;
+}
+
+}  // namespace
+
+extern "C" int32_t ffb_classify_opcodes(FfbContext* ctx, const uint8_t* d_text, const int64_t* d_off, int64_t n,
+                                        uint32_t* d_out, void* stream) {
+  if (!ctx || !d_text || !d_off || !d_out || n < 0) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_classify_opcodes: bad argument");
+  if (n == 0) return FFB_OK;
+  FFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  FFB_LAUNCH(classify_opcodes_kernel, (unsigned)((n + 255) / 256), 256, 0, stream, d_text, d_off, n, d_out);
+  return ffb_check_launch(ctx, "classify_opcodes_kernel");
+}
+
+namespace {
 }  // namespace
 
 extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream_) {
@@ -1119,7 +1153,7 @@ extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* st
   a.hist = d->d_hist; a.info = d->d_info;
   a.ins_base = d->d_ins_base; a.lab_base = d->d_lab_base;
   a.ins = (FfbInsRec*)d->d_ins; a.labels = (FfbLabelRec*)d->d_labels;
-  a.spans = d->d_spans; a.decls = d->d_decls;
+  a.spans = d->d_spans; a.decls = d->d_decls; a.meta = d->d_meta;
   a.want_name = nullptr; a.want_len = 0;
   if (d->h_kernel_name && d->kernel_name_len > 0) {
     if (d->kernel_name_len > 2048) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_lex_corpus: kernel name too long");

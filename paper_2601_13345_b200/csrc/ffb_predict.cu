@@ -36,6 +36,7 @@ struct Tables {
   const double* cap_scale; // [S, C]  f_adj / f_base
   const double* cap_fadj;  // [S, C]
   const double* cap_ok;    // [S, C]  1.0 when p_cap_min <= cap <= p_tdp
+  const double* cap_tab;   // [S, C, 4] {scale, cap, max(0, cap - p_static), ok}: the cap axis in one 32-byte row
   const double* psm;       // [S, psm_n]
   int psm_n;
 };
@@ -109,7 +110,8 @@ struct GridArgs {
   int strict;
 };
 
-template <bool kDetail>
+// kLean: only t / e requested and no strict checks — the streaming configuration
+template <bool kDetail, bool kLean>
 __global__ void __launch_bounds__(kUnitsPerCta)
 predict_grid_kernel(GridArgs a) {
   FFB_DYN_SMEM(smem_raw);
@@ -124,10 +126,16 @@ predict_grid_kernel(GridArgs a) {
   const bool live = unit < a.n_units;
 
   if (live) {
-    const int64_t ks = unit / a.n_shapes;
-    const int j = (int)(unit - ks * a.n_shapes);
-    const int64_t k = ks / a.n_specs;
-    const int s = (int)(ks - k * a.n_specs);
+    int64_t ks, k;
+    int j, s;
+    if (a.n_units <= 0x7fffffffLL) {                   // 32-bit index arithmetic on the common sizes
+      const uint32_t u32 = (uint32_t)unit, ks32 = u32 / (uint32_t)a.n_shapes, k32 = ks32 / (uint32_t)a.n_specs;
+      j = (int)(u32 - ks32 * (uint32_t)a.n_shapes); s = (int)(ks32 - k32 * (uint32_t)a.n_specs);
+      ks = ks32; k = k32;
+    } else {
+      ks = unit / a.n_shapes; j = (int)(unit - ks * a.n_shapes);
+      k = ks / a.n_specs; s = (int)(ks - k * a.n_specs);
+    }
     const double* f = a.feat + k * FFB_FEAT_WIDTH;
     const double* sp = a.tb.spec + (size_t)s * FFB_SPEC_WIDTH;
     const double* sd = a.tb.sd + (size_t)s * kSdWidth;
@@ -203,27 +211,28 @@ predict_grid_kernel(GridArgs a) {
     const double p_static = sp[FFB_S_P_STATIC];
     const double e_over = sp[FFB_S_E_OVERHEAD];
 
-    if (a.occ) a.occ[unit] = bps;
-    if (err && a.status) atomicOr(a.status, err);
+    if (!kLean) {
+      if (a.occ) a.occ[unit] = bps;
+      if (err && a.status) atomicOr(a.status, err);
+    }
 
     // ---- cap axis (power_model.py:152-158, explorer.py:107) ----
-    const double* cscale = a.tb.cap_scale + (size_t)s * C;
-    const double* cok = a.tb.cap_ok + (size_t)s * C;
+    const double2* ct = reinterpret_cast<const double2*>(a.tb.cap_tab + (size_t)s * C * 4);
+    const bool any_cap = kLean ? false : (a.strict != 0);
     for (int c = 0; c < C; ++c) {
-      const double cap = a.tb.cap[c];
-      double p_dyn = p_pre * cscale[c];
-      bool limited = false;
-      if (p_dyn + p_static > cap) {
-        p_dyn = py_max(0.0, cap - p_static);
-        limited = true;
-      }
+      const double2 sc_cap = ct[2 * c], room_ok = ct[2 * c + 1];
+      double p_dyn = p_pre * sc_cap.x;
+      const bool limited = p_dyn + p_static > sc_cap.y;
+      if (limited) p_dyn = room_ok.x;                       // max(0.0, cap - p_static), tabulated
       const double e_pred = t_exec * (p_dyn + p_static) + e_over;
-      const bool ok = unit_valid && (a.strict || cok[c] != 0.0);
+      const bool ok = unit_valid && (any_cap || room_ok.y != 0.0);
       const size_t o = (size_t)threadIdx.x * C + c;
       s_t[o] = ok ? t_exec : INFINITY;
       s_e[o] = ok ? e_pred : INFINITY;
-      if (a.pdyn) s_p[o] = p_dyn;
-      if (a.flags) s_f[o] = (uint8_t)((ok ? FFB_PT_VALID : 0) | (limited ? FFB_PT_CAP_LIMITED : 0));
+      if (!kLean) {
+        if (a.pdyn) s_p[o] = p_dyn;
+        if (a.flags) s_f[o] = (uint8_t)((ok ? FFB_PT_VALID : 0) | (limited ? FFB_PT_CAP_LIMITED : 0));
+      }
       if (kDetail) {
         double* d = a.detail + ((size_t)unit * C + c) * FFB_DETAIL_WIDTH;
         d[FFB_D_MWP] = mwp; d[FFB_D_CWP] = kr[KS_CWP]; d[FFB_D_BW_EFF] = bw_eff;
@@ -244,11 +253,24 @@ predict_grid_kernel(GridArgs a) {
   const int n_live = rem < kUnitsPerCta ? (int)rem : kUnitsPerCta;
   const size_t base = (size_t)unit0 * C;
   const int total = n_live * C;
-  for (int i = threadIdx.x; i < total; i += kUnitsPerCta) {
-    if (a.t) a.t[base + i] = s_t[i];
-    if (a.e) a.e[base + i] = s_e[i];
-    if (a.pdyn) a.pdyn[base + i] = s_p[i];
-    if (a.flags) a.flags[base + i] = s_f[i];
+  if (kLean && (base & 1) == 0) {
+    // 16-byte stores: the tile starts on an even element, so (t + base) is 16-byte aligned
+    const int pairs = total >> 1;
+    double2* gt = reinterpret_cast<double2*>(a.t + base);
+    double2* ge = reinterpret_cast<double2*>(a.e + base);
+    const double2* st2 = reinterpret_cast<const double2*>(s_t);
+    const double2* se2 = reinterpret_cast<const double2*>(s_e);
+    for (int i = threadIdx.x; i < pairs; i += kUnitsPerCta) { gt[i] = st2[i]; ge[i] = se2[i]; }
+    if ((total & 1) && threadIdx.x == 0) { a.t[base + total - 1] = s_t[total - 1]; a.e[base + total - 1] = s_e[total - 1]; }
+  } else {
+    for (int i = threadIdx.x; i < total; i += kUnitsPerCta) {
+      if (a.t) a.t[base + i] = s_t[i];
+      if (a.e) a.e[base + i] = s_e[i];
+      if (!kLean) {
+        if (a.pdyn) a.pdyn[base + i] = s_p[i];
+        if (a.flags) a.flags[base + i] = s_f[i];
+      }
+    }
   }
 }
 
@@ -302,7 +324,7 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   }
   const size_t n_spec = (size_t)S * FFB_SPEC_WIDTH, n_sd = (size_t)S * kSdWidth, n_log = (size_t)J,
                n_cap = (size_t)C, n_sc = (size_t)S * C, n_psm = (size_t)S * psm_n;
-  const size_t n_dbl = n_spec + n_sd + n_log + n_cap + 3 * n_sc + n_psm;
+  const size_t n_dbl = n_spec + n_sd + n_log + n_cap + 7 * n_sc + n_psm;
   const size_t bytes = n_dbl * sizeof(double) + (size_t)J * 4 * sizeof(int32_t);
   int32_t rc = ffb_stage_reserve(ctx, bytes);
   if (rc) return rc;
@@ -316,7 +338,8 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   double* h_scale = h_cap + n_cap;
   double* h_fadj = h_scale + n_sc;
   double* h_ok = h_fadj + n_sc;
-  double* h_psm = h_ok + n_sc;
+  double* h_ctab = h_ok + n_sc;
+  double* h_psm = h_ctab + 4 * n_sc;
   int32_t* h_shape = (int32_t*)(h_psm + n_psm);
   memcpy(h_spec, g->h_spec, n_spec * sizeof(double));
   memcpy(h_cap, g->h_cap, n_cap * sizeof(double));
@@ -337,6 +360,8 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
       h_fadj[s * C + c] = fadj;
       h_scale[s * C + c] = fadj / fb;                                          // power_model.py:153
       h_ok[s * C + c] = in_range ? 1.0 : 0.0;
+      double* row = h_ctab + (s * C + c) * 4;
+      row[0] = fadj / fb; row[1] = cap; row[2] = py_max(0.0, cap - sp[FFB_S_P_STATIC]); row[3] = in_range ? 1.0 : 0.0;   // power_model.py:157
     }
     const double al = sp[FFB_S_SM_ALPHA], be = sp[FFB_S_SM_BETA], de = sp[FFB_S_SM_DELTA];
     h_psm[s * psm_n + 0] = de;                                                 // power_model.py:74-75
@@ -360,7 +385,8 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   tb.cap_scale = tb.cap + n_cap;
   tb.cap_fadj = tb.cap_scale + n_sc;
   tb.cap_ok = tb.cap_fadj + n_sc;
-  tb.psm = tb.cap_ok + n_sc;
+  tb.cap_tab = tb.cap_ok + n_sc;
+  tb.psm = tb.cap_tab + 4 * n_sc;
   tb.shape = (const int32_t*)(tb.psm + n_psm);
   tb.psm_n = psm_n;
 
@@ -384,12 +410,16 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
     return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_predict_grid: %lld caps exceed the shared-memory tile", (long long)C);
   const int64_t n_cta = (a.n_units + kUnitsPerCta - 1) / kUnitsPerCta;
   if (n_cta > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_predict_grid: grid too large for one launch");
+  const bool lean = !g->d_detail && !g->d_pdyn && !g->d_flags && !g->d_occ && !g->strict && !g->d_status && g->d_t && g->d_e;
   if (g->d_detail) {
-    FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FFB_LAUNCH(predict_grid_kernel<true>, (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
+    FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FFB_LAUNCH((predict_grid_kernel<true, false>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
+  } else if (lean) {
+    FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FFB_LAUNCH((predict_grid_kernel<false, true>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
   } else {
-    FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FFB_LAUNCH(predict_grid_kernel<false>, (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
+    FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FFB_LAUNCH((predict_grid_kernel<false, false>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
   }
   rc = ffb_check_launch(ctx, "predict_grid_kernel");
   if (rc) return rc;

@@ -53,6 +53,7 @@ _SIGNATURES = {
     "ffb_skyline_groups": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "ffb_lex_corpus": (_i32, [_vp, _vp, _vp]),
     "ffb_kernel_features": (_i32, [_vp, _vp, _vp]),
+    "ffb_classify_opcodes": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "ffb_name_hash": (C.c_uint64, [C.c_char_p, _i64]),
     "ffb_skyline": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _f64, _vp, _vp, _vp, _i64,
                            C.POINTER(_i64), C.POINTER(_f64), _vp]),

@@ -145,9 +145,9 @@ def test_model_helpers_known_answers(backend):
 
 def test_classifier_and_errors(backend):
     table = json.loads((G / "ref_classify.json").read_text())
-    ops = list(table)[: (len(table) if backend == "gpu" else 12)]
-    for op in ops:
-        assert list(api.classify_opcode(op)) == table[op][:2], op
+    ops = list(table)
+    assert [list(x) for x in api.classify_opcodes(ops)] == [table[op] for op in ops]
+    assert list(api.classify_opcode("ld.global.v4.f32")) == ["MemLoad", "global"]
     a = specs.default_architecture()
     with pytest.raises(E.SharedMemOverflow):
         api.compute_input_resources(100000, 1, 1, 64, 4, a)

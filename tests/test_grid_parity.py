@@ -100,3 +100,17 @@ def test_detail_rows_and_strict_errors(backend):
     with pytest.raises(EmptyGrid):
         engine.score_grid(engine.features_tensor(feat), engine.resources_tensor(res0), sp, shp,
                           np.array([150.0]), strict=True)
+
+
+def test_lean_streaming_path_matches_checked_path(backend):
+    """check=False + (t, e) only selects the lean kernel variant (vector stores, no status)."""
+    K = 5 if backend == "emul" else 1500
+    feat, res = synth.feature_rows(seed=21, n_kernels=K)
+    sp = engine.spec_rows([(specs.default_architecture(), specs.default_calibration()), _alt_spec()])
+    shp = engine.shape_rows([tuple(x) for x in engine.enumerate_shapes(sp[0], 0, [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024])])
+    for caps in (np.array([100.0, 150.0, 200.0, 250.0, 275.0]), np.array([125.0, 225.0])):
+        f, r_ = engine.features_tensor(feat), engine.resources_tensor(res)
+        full = engine.score_grid(f, r_, sp, shp, caps, want=("t", "e", "flags"))
+        lean = engine.score_grid(f, r_, sp, shp, caps, want=("t", "e"), check=False)
+        assert torch.equal(full.t.view(torch.int64), lean.t.view(torch.int64))
+        assert torch.equal(full.e.view(torch.int64), lean.e.view(torch.int64))
