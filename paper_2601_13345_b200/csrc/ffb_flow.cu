@@ -30,7 +30,8 @@
 
 namespace {
 
-constexpr int kFlowThreads = 64;
+constexpr int kFlowWarps = 4;
+constexpr int kCacheSlots = 256;
 constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
 constexpr uint32_t kNoBlock = 0xffffffffu;
@@ -44,6 +45,7 @@ struct FlowArgs {
   const FfbLabelRec* labels;
   const uint32_t* meta_arr;     // optional compact meta words
   const int32_t* order;
+  unsigned long long* work;     // work-queue counter
   double default_trip;
   const uint64_t* ann_hash;     // device copies
   const double* ann_trip;
@@ -186,375 +188,533 @@ FFB_D bool dominates(const int32_t* idom, const int32_t* rpo_num, uint32_t h, ui
   }
 }
 
-__global__ void __launch_bounds__(kFlowThreads)
+// ---- warp helpers -----------------------------------------------------------------------------------
+constexpr unsigned kAll = 0xffffffffu;
+FFB_D int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) { const int64_t o = __shfl_xor_sync(kAll, v, d); v = o > v ? o : v; }
+  return v;
+}
+FFB_D int warp_sum_i(int v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kAll, v, d);
+  return v;
+}
+
+// Write-through cache of the register -> scale table in shared memory (direct mapped).  Most
+// sources were defined a few statements earlier, so most look-ups never leave the SM.
+struct CachedScales {
+  ScaleTable g;
+  uint64_t* ckey; int64_t* cval;
+  FFB_D int64_t get(uint64_t h) {
+    const uint32_t c = (uint32_t)(h ^ (h >> 17)) & (kCacheSlots - 1);
+    if (ckey[c] == h + 1) return cval[c];
+    const int64_t v = g.get(h);
+    ckey[c] = h + 1; cval[c] = v;
+    return v;
+  }
+  FFB_D void put(uint64_t h, int64_t v) {
+    const uint32_t c = (uint32_t)(h ^ (h >> 17)) & (kCacheSlots - 1);
+    ckey[c] = h + 1; cval[c] = v;
+    g.put(h, v);
+  }
+};
+FFB_D int64_t operand_scale_c(uint64_t d, CachedScales& t) {
+  switch (ffb_op_kind(d)) {
+    case FFB_OPK_TIDX: return 1;
+    case FFB_OPK_UNKNOWN: return kNoneScale;
+    case FFB_OPK_REG: return t.get(ffb_op_hash(d));
+    case FFB_OPK_NONE: return kNoneScale;
+    default: return 0;
+  }
+}
+FFB_D int64_t mul_scale_c(uint64_t a, uint64_t b, CachedScales& t) {
+  const int64_t sa = operand_scale_c(a, t), sb = operand_scale_c(b, t);
+  if (sa == 0 && sb == 0) return 0;
+  if (is_int_lit(b) && sc_known(sa)) return sc_mul(sa, int_as_scale(b));
+  if (is_int_lit(a) && sc_known(sb)) return sc_mul(int_as_scale(a), sb);
+  return kNoneScale;
+}
+
+// One WARP per kernel.  Lane-parallel: label table, leaders, block numbering, edges, the
+// "last match" scans of the trip recogniser, weights, record staging.  Lane 0 alone: the graph
+// walks (DFS, dominators, loop bodies) and the textual dataflow pass, which are sequential by
+// nature; it reads the records from a 32-entry shared-memory stage the whole warp fills.
+__global__ void __launch_bounds__(kFlowWarps * 32)
 flow_kernel(FlowArgs a) {
-  const int64_t w = (int64_t)blockIdx.x * kFlowThreads + threadIdx.x;
-  if (w >= a.n_segs) return;
-  const int64_t k = a.order ? (int64_t)a.order[w] : w;
-  const FfbSegInfo inf = a.info[k];
-  double* feat = a.feat + k * FFB_FEAT_WIDTH;
-  for (int c = 0; c < FFB_FEAT_WIDTH; ++c) feat[c] = 0.0;
-  feat[FFB_F_OVR_TEXEC] = NAN;
-  uint32_t status = inf.status;
-  FfbFlowInfo fi;
-  fi.n_blocks = fi.n_edges = fi.n_loops = 0; fi.reserved = 0;
-  if (status != FFB_OK) { a.status[k] = status; if (a.flow) a.flow[k] = fi; return; }
+  __shared__ FfbInsRec s_stage[kFlowWarps][32];      // FfbInsRec is 16-byte aligned by declaration
+  __shared__ double s_wstage[kFlowWarps][32];
+  __shared__ uint64_t s_ckey[kFlowWarps][kCacheSlots];
+  __shared__ int64_t s_cval[kFlowWarps][kCacheSlots];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  FfbInsRec* stage = s_stage[wid];
+  double* wstage = s_wstage[wid];
 
-  const uint32_t n = inf.n_instr, L = inf.n_labels;
-  const int64_t ib = a.ins_base[k], lb = a.lab_base[k];
-  const FfbInsRec* ins = a.ins + ib;
-  const FfbLabelRec* lab = a.labels + lb;
-  const uint32_t* cm = a.meta_arr ? a.meta_arr + ib : nullptr;        // compact meta stream
+  for (;;) {
+    unsigned long long w = 0;
+    if (lane == 0) w = atomicAdd(a.work, 1ull);
+    w = __shfl_sync(kAll, w, 0);
+    if (w >= (unsigned long long)a.n_segs) break;
+    const int64_t k = a.order ? (int64_t)a.order[w] : (int64_t)w;
+    const FfbSegInfo inf = a.info[k];
+    double* feat = a.feat + k * FFB_FEAT_WIDTH;
+    if (lane < FFB_FEAT_WIDTH) feat[lane] = lane == FFB_F_OVR_TEXEC ? NAN : 0.0;
+    uint32_t status = inf.status;
+    FfbFlowInfo fi;
+    fi.n_blocks = fi.n_edges = fi.n_loops = 0; fi.reserved = 0;
+    if (status != FFB_OK) {
+      if (lane == 0) { a.status[k] = status; if (a.flow) a.flow[k] = fi; }
+      continue;
+    }
+    const uint32_t n = inf.n_instr, L = inf.n_labels;
+    const int64_t ib = a.ins_base[k], lb = a.lab_base[k];
+    const FfbInsRec* ins = a.ins + ib;
+    const FfbLabelRec* lab = a.labels + lb;
+    const uint32_t* cm = a.meta_arr ? a.meta_arr + ib : nullptr;        // compact meta stream
 #define FFB_META(i) (cm ? cm[i] : ins[i].meta)
-  const int64_t o1 = ib + 2 * k;                   // offset into the [N + 2K] arrays
-  uint32_t* block_of = a.block_of + ib;
-  uint32_t* block_start = a.block_start + o1;
-  int32_t* succ0 = a.succ0 + o1;
-  int32_t* succ1 = a.succ1 + o1;
-  uint32_t* pred_ptr = a.pred_ptr + o1;
-  uint32_t* pred_list = a.pred_list + 2 * o1;
-  int32_t* rpo_num = a.rpo_num + o1;
-  uint32_t* rpo_order = a.rpo_order + o1;
-  int32_t* idom = a.idom + o1;
-  uint32_t* mark = a.mark + o1;
-  uint32_t* stack = a.stack + o1;
-  double* weight = a.weight + o1;
-  LabelTable lt;
-  lt.key = a.lab_key + 4 * lb + 8 * k; lt.first = a.lab_first + 4 * lb + 8 * k; lt.last = a.lab_last + 4 * lb + 8 * k;
-  lt.cap = 4; while (lt.cap < 2 * L + 2) lt.cap <<= 1;          // <= 4L + 8
-  ScaleTable st;
-  st.key = a.sc_key + 4 * ib + 8 * k; st.val = a.sc_val + 4 * ib + 8 * k;
-  st.cap = 4; while (st.cap < 2 * n + 2) st.cap <<= 1;          // <= 4n + 8
+    const int64_t o1 = ib + 2 * k;                   // offset into the [N + 2K] arrays
+    uint32_t* block_of = a.block_of + ib;
+    uint32_t* block_start = a.block_start + o1;
+    int32_t* succ0 = a.succ0 + o1;
+    int32_t* succ1 = a.succ1 + o1;
+    uint32_t* pred_ptr = a.pred_ptr + o1;
+    uint32_t* pred_list = a.pred_list + 2 * o1;
+    int32_t* rpo_num = a.rpo_num + o1;
+    uint32_t* rpo_order = a.rpo_order + o1;
+    int32_t* idom = a.idom + o1;
+    uint32_t* mark = a.mark + o1;
+    uint32_t* stack = a.stack + o1;
+    double* weight = a.weight + o1;
+    LabelTable lt;
+    lt.key = a.lab_key + 4 * lb + 8 * k; lt.first = a.lab_first + 4 * lb + 8 * k; lt.last = a.lab_last + 4 * lb + 8 * k;
+    lt.cap = 4; while (lt.cap < 2 * L + 2) lt.cap <<= 1;          // <= 4L + 8
+    CachedScales st;
+    st.g.key = a.sc_key + 4 * ib + 8 * k; st.g.val = a.sc_val + 4 * ib + 8 * k;
+    st.g.cap = 4; while (st.g.cap < 2 * n + 2) st.g.cap <<= 1;      // <= 4n + 8
+    st.ckey = s_ckey[wid]; st.cval = s_cval[wid];
 
-  // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
-  lt.clear();
-  for (uint32_t i = 0; i < L; ++i) lt.define(lab[i].hash, i, 0);
-  // ---- leaders (cfg.py:63-70); block_of doubles as the leader flag array first ----
-  for (uint32_t i = 0; i < n; ++i) block_of[i] = 0;
-  block_of[0] = 1;
-  for (uint32_t i = 0; i < L; ++i) {
-    const uint32_t s = lt.find(lab[i].hash);
-    if (lt.last[s] == i && lab[i].index < n) block_of[lab[i].index] = 1;     // effective definition only
-  }
-  for (uint32_t i = 0; i + 1 < n; ++i) {
-    const uint32_t m = FFB_META(i);
-    const uint32_t base = ffb_meta_base(m);
-    if (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT) block_of[i + 1] = 1;
-  }
-  uint32_t nb = 0;
-  for (uint32_t i = 0; i < n; ++i) {
-    if (block_of[i]) block_start[nb++] = i;
-    block_of[i] = nb - 1;
-  }
-  block_start[nb] = n;
-  // ---- edges (cfg.py:80-92) and branch-target validation (ptx.py:277-284) ----
-  uint32_t n_edges = 0;
-  for (uint32_t b = 0; b < nb; ++b) { succ0[b] = -1; succ1[b] = -1; pred_ptr[b] = 0; }
-  pred_ptr[nb] = 0;
-  for (uint32_t i = 0; i < n && status == FFB_OK; ++i) {
-    const uint32_t m = FFB_META(i);
-    if (ffb_meta_cls(m) != FFB_CLS_BRANCH) continue;
-    const uint64_t tgt = ins[i].aux;
-    const uint32_t s = tgt ? lt.find(ffb_op_hash(tgt)) : lt.cap;
-    if (s == lt.cap) status = FFB_E_MALFORMED_PTX;
-  }
-  if (status != FFB_OK) { a.status[k] = status; if (a.flow) a.flow[k] = fi; return; }
-  for (uint32_t b = 0; b < nb; ++b) {
-    const FfbInsRec& last = ins[block_start[b + 1] - 1];
-    const uint32_t m = FFB_META(block_start[b + 1] - 1);
-    const uint32_t base = ffb_meta_base(m);
-    if (ffb_meta_cls(m) == FFB_CLS_BRANCH) {
-      const uint32_t s = lt.find(ffb_op_hash(last.aux));
-      const uint32_t tidx = lab[lt.last[s]].index;
-      if (tidx < n) succ0[b] = (int32_t)block_of[tidx];
-      if (ffb_meta_has_pred(m) && b + 1 < nb) succ1[b] = (int32_t)(b + 1);
-    } else if (base == FFB_BASE_RET || base == FFB_BASE_EXIT) {
-    } else if (b + 1 < nb) {
-      succ1[b] = (int32_t)(b + 1);
-    }
-    if (succ0[b] >= 0) { ++n_edges; ++pred_ptr[succ0[b] + 1]; }
-    if (succ1[b] >= 0) { ++n_edges; ++pred_ptr[succ1[b] + 1]; }
-  }
-  for (uint32_t b = 0; b < nb; ++b) pred_ptr[b + 1] += pred_ptr[b];
-  for (uint32_t b = 0; b < nb; ++b) mark[b] = pred_ptr[b];           // fill cursors
-  for (uint32_t b = 0; b < nb; ++b) {                                // edge order = (b, branch) then (b, fallthrough)
-    if (succ0[b] >= 0) pred_list[mark[succ0[b]]++] = b;
-    if (succ1[b] >= 0) pred_list[mark[succ1[b]]++] = b;
-  }
-  // ---- reverse post-order from block 0 (iterative DFS) ----
-  for (uint32_t b = 0; b < nb; ++b) { rpo_num[b] = -1; mark[b] = 0; idom[b] = -1; }
-  uint32_t post = 0, sp = 0;
-  stack[sp++] = 0; mark[0] = 1;            // mark: 0 unseen, 1 = next child is succ0, 2 = succ1, 3 = done
-  while (sp) {
-    const uint32_t b = stack[sp - 1];
-    int32_t child = -1;
-    while (mark[b] < 3 && child < 0) {
-      const int32_t c = mark[b] == 1 ? succ0[b] : succ1[b];
-      ++mark[b];
-      if (c >= 0 && mark[c] == 0) child = c;
-    }
-    if (child >= 0) { mark[child] = 1; stack[sp++] = (uint32_t)child; }
-    else { rpo_order[post++] = b; --sp; }
-  }
-  const uint32_t n_reach = post;
-  for (uint32_t i = 0; i < n_reach; ++i) rpo_num[rpo_order[i]] = (int32_t)(n_reach - 1 - i);   // 0 = entry
-  // ---- immediate dominators (Cooper-Harvey-Kennedy) ----
-  idom[0] = 0;
-  for (bool changed = true; changed;) {
-    changed = false;
-    for (int32_t r = (int32_t)n_reach - 2; r >= 0; --r) {            // reverse post-order, entry skipped
-      const uint32_t b = rpo_order[r];
-      int32_t nd = -1;
-      for (uint32_t p = pred_ptr[b]; p < pred_ptr[b + 1]; ++p) {
-        const uint32_t q = pred_list[p];
-        if (rpo_num[q] < 0 || idom[q] < 0) continue;
-        if (nd < 0) { nd = (int32_t)q; continue; }
-        int32_t x = (int32_t)q, y = nd;
-        while (x != y) {
-          while (rpo_num[x] > rpo_num[y]) x = idom[x];
-          while (rpo_num[y] > rpo_num[x]) y = idom[y];
-        }
-        nd = x;
+    // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
+    for (uint32_t i = lane; i < lt.cap; i += 32) { lt.key[i] = 0; lt.first[i] = 0xffffffffu; lt.last[i] = 0; }
+    for (uint32_t i = lane; i < st.g.cap; i += 32) st.g.key[i] = 0;
+    for (uint32_t i = lane; i < kCacheSlots; i += 32) st.ckey[i] = 0;
+    for (uint32_t i = lane; i < n; i += 32) block_of[i] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < L; i += 32) {
+      const uint64_t key = lab[i].hash + 1;
+      uint32_t s = slot_of(lab[i].hash, lt.cap);
+      for (;;) {
+        const unsigned long long prev = atomicCAS((unsigned long long*)&lt.key[s], 0ull, (unsigned long long)key);
+        if (prev == 0ull || prev == key) break;
+        s = (s + 1) & (lt.cap - 1u);
       }
-      if (nd != idom[b]) { idom[b] = nd; changed = true; }
+      atomicMin(&lt.first[s], i);
+      atomicMax(&lt.last[s], i);
     }
-  }
-  // ---- natural loops, one per header in ascending header order (cfg.py:124-151) ----
-  for (uint32_t b = 0; b < nb; ++b) { weight[b] = 1.0; mark[b] = 0; }
-  uint32_t n_loops = 0;
-  for (uint32_t h = 0; h < nb; ++h) {
-    // back edges into h: predecessors u with h in dom(u)
-    bool is_header = false;
-    const uint32_t stamp = h + 1;
-    for (uint32_t p = pred_ptr[h]; p < pred_ptr[h + 1]; ++p) {
-      const uint32_t u = pred_list[p];
-      if (!dominates(idom, rpo_num, h, u)) continue;
-      is_header = true;
-      // body = {h, u} + everything that reaches u without passing h
-      mark[h] = stamp;
-      if (mark[u] != stamp) { mark[u] = stamp; }
-      uint32_t top = 0;
-      stack[top++] = u;
-      while (top) {
-        const uint32_t x = stack[--top];
-        if (x == h) continue;
-        for (uint32_t q = pred_ptr[x]; q < pred_ptr[x + 1]; ++q) {
-          const uint32_t y = pred_list[q];
-          if (mark[y] != stamp) { mark[y] = stamp; stack[top++] = y; }
-        }
-      }
-    }
-    if (!is_header) continue;
-    const uint32_t h0 = block_start[h];
-    // header label: the dictionary's last name that maps to the header's first instruction
-    uint64_t hl_hash = 0; uint32_t hl_off = 0; bool hl_any = false; uint32_t hl_order = 0;
-    for (uint32_t i = 0; i < L; ++i) {
+    __syncwarp();
+    // ---- leaders (cfg.py:63-70); block_of doubles as the flag array first ----
+    for (uint32_t i = lane; i < L; i += 32) {
       const uint32_t s = lt.find(lab[i].hash);
-      if (lt.last[s] != i || lab[i].index != h0) continue;       // only effective definitions
-      const uint32_t ord = lt.first[s];
-      if (!hl_any || ord >= hl_order) { hl_any = true; hl_order = ord; hl_hash = lab[i].hash; hl_off = lab[lt.first[s]].off; }
+      if (lt.last[s] == i && lab[i].index < n) block_of[lab[i].index] = 1;     // effective definition only
     }
-    // ---- trip count ----
-    double trip = -1.0;
-    bool annotated = false;
-    if (hl_any) {
-      for (int q = 0; q < a.n_ann; ++q)
-        if (a.ann_hash[q] == hl_hash) { trip = a.ann_trip[q]; annotated = true; if (a.ann_hit) a.ann_hit[q] = 1; }
+    for (uint32_t i = lane; i + 1 < n; i += 32) {
+      const uint32_t m = FFB_META(i);
+      const uint32_t base = ffb_meta_base(m);
+      if (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT) block_of[i + 1] = 1;
     }
-    if (!annotated) {
-      // cfg.py:191-279
-      bool ok = true;
-      int64_t latch = -1;
-      for (uint32_t b = 0; b < nb; ++b) {
-        if (mark[b] != stamp) continue;
-        for (uint32_t i = block_start[b]; i < block_start[b + 1]; ++i) {
-          const uint32_t m = FFB_META(i);
-          if (ffb_meta_cls(m) == FFB_CLS_BRANCH && ffb_meta_has_pred(m)) {
-            const uint32_t s = lt.find(ffb_op_hash(ins[i].aux));
-            if (lab[lt.last[s]].index == h0) latch = i;
+    if (lane == 0) block_of[0] = 1;
+    __syncwarp();
+    uint32_t nb = 0;
+    for (uint32_t c = 0; c < n; c += 32) {
+      const uint32_t i = c + lane;
+      const bool f = i < n && block_of[i] != 0;
+      const unsigned mask = __ballot_sync(kAll, f);
+      const uint32_t id = nb + __popc(mask & (0xffffffffu >> (31 - lane))) - 1;   // leaders at or before me
+      if (i < n) block_of[i] = id;
+      if (f) block_start[id] = i;
+      nb += __popc(mask);
+    }
+    if (lane == 0) block_start[nb] = n;
+    for (uint32_t b = lane; b <= nb; b += 32) { pred_ptr[b] = 0; }
+    __syncwarp();
+    // ---- edges (cfg.py:80-92) and branch-target validation (ptx.py:277-284) ----
+    bool bad_target = false;
+    for (uint32_t b = lane; b < nb; b += 32) {
+      const uint32_t li = block_start[b + 1] - 1;
+      const uint32_t m = FFB_META(li);
+      const uint32_t base = ffb_meta_base(m);
+      int32_t t0 = -1, t1 = -1;
+      if (ffb_meta_cls(m) == FFB_CLS_BRANCH) {
+        const uint64_t tgt = ins[li].aux;
+        const uint32_t s = tgt ? lt.find(ffb_op_hash(tgt)) : lt.cap;
+        if (s == lt.cap) bad_target = true;
+        else {
+          const uint32_t tidx = lab[lt.last[s]].index;
+          if (tidx < n) t0 = (int32_t)block_of[tidx];
+          if (ffb_meta_has_pred(m) && b + 1 < nb) t1 = (int32_t)(b + 1);
+        }
+      } else if (base == FFB_BASE_RET || base == FFB_BASE_EXIT) {
+      } else if (b + 1 < nb) {
+        t1 = (int32_t)(b + 1);
+      }
+      succ0[b] = t0; succ1[b] = t1;
+      if (t0 >= 0) atomicAdd(&pred_ptr[t0 + 1], 1u);
+      if (t1 >= 0) atomicAdd(&pred_ptr[t1 + 1], 1u);
+    }
+    if (__any_sync(kAll, bad_target)) {
+      if (lane == 0) { a.status[k] = FFB_E_MALFORMED_PTX; if (a.flow) a.flow[k] = fi; }
+      continue;
+    }
+    __syncwarp();
+    uint32_t n_edges = 0;
+    {   // inclusive scan of pred_ptr[1..nb] in chunks of 32
+      uint32_t carry = 0;
+      for (uint32_t c = 1; c <= nb; c += 32) {
+        const uint32_t i = c + lane;
+        uint32_t v = i <= nb ? pred_ptr[i] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { const uint32_t o = __shfl_up_sync(kAll, v, d); if (lane >= d) v += o; }
+        if (i <= nb) pred_ptr[i] = v + carry;
+        carry += __shfl_sync(kAll, v, 31);
+      }
+      n_edges = carry;
+    }
+    __syncwarp();
+    for (uint32_t b = lane; b < nb; b += 32) mark[b] = pred_ptr[b];          // fill cursors
+    __syncwarp();
+    for (uint32_t b = lane; b < nb; b += 32) {
+      if (succ0[b] >= 0) pred_list[atomicAdd(&mark[succ0[b]], 1u)] = b;
+      if (succ1[b] >= 0) pred_list[atomicAdd(&mark[succ1[b]], 1u)] = b;
+    }
+    for (uint32_t b = lane; b < nb; b += 32) { rpo_num[b] = -1; idom[b] = -1; weight[b] = 1.0; }
+    __syncwarp();
+    for (uint32_t b = lane; b < nb; b += 32) mark[b] = 0;
+    __syncwarp();
+    // ---- lane 0: reverse post-order from block 0 and immediate dominators ----
+    if (lane == 0) {
+      uint32_t post = 0, sp = 0;
+      stack[sp++] = 0; mark[0] = 1;          // mark: 0 unseen, 1 = next child is succ0, 2 = succ1, 3 = done
+      while (sp) {
+        const uint32_t b = stack[sp - 1];
+        int32_t child = -1;
+        while (mark[b] < 3 && child < 0) {
+          const int32_t c = mark[b] == 1 ? succ0[b] : succ1[b];
+          ++mark[b];
+          if (c >= 0 && mark[c] == 0) child = c;
+        }
+        if (child >= 0) { mark[child] = 1; stack[sp++] = (uint32_t)child; }
+        else { rpo_order[post++] = b; --sp; }
+      }
+      const uint32_t n_reach = post;
+      for (uint32_t i = 0; i < n_reach; ++i) rpo_num[rpo_order[i]] = (int32_t)(n_reach - 1 - i);   // 0 = entry
+      idom[0] = 0;
+      for (bool changed = true; changed;) {
+        changed = false;
+        for (int32_t r = (int32_t)n_reach - 2; r >= 0; --r) {            // reverse post-order, entry skipped
+          const uint32_t b = rpo_order[r];
+          int32_t nd = -1;
+          for (uint32_t p = pred_ptr[b]; p < pred_ptr[b + 1]; ++p) {
+            const uint32_t q = pred_list[p];
+            if (rpo_num[q] < 0 || idom[q] < 0) continue;
+            if (nd < 0) { nd = (int32_t)q; continue; }
+            int32_t x = (int32_t)q, y = nd;
+            while (x != y) {
+              while (rpo_num[x] > rpo_num[y]) x = idom[x];
+              while (rpo_num[y] > rpo_num[x]) y = idom[y];
+            }
+            nd = x;
           }
+          if (nd != idom[b]) { idom[b] = nd; changed = true; }
         }
       }
-      int64_t cmp_i = -1;
-      if (latch < 0) ok = false;
-      if (ok) {
-        const uint64_t preg = ins[latch].pred;
-        for (uint32_t b = 0; b < nb; ++b) {
-          if (mark[b] != stamp) continue;
-          for (uint32_t i = block_start[b]; i < block_start[b + 1]; ++i) {
-            const uint32_t m = FFB_META(i);
-            if (ffb_meta_base(m) == FFB_BASE_SETP && ffb_meta_nops(m) >= 1 && ffb_op_kind(ins[i].op[0]) != FFB_OPK_INT &&
-                ffb_op_hash(ins[i].op[0]) == preg) cmp_i = i;
-          }
-        }
-        if (cmp_i < 0 || ffb_meta_nops(ins[cmp_i].meta) < 3) ok = false;
-      }
-      uint64_t counter = 0; int64_t bound = 0; uint32_t rel = FFB_CMP_NONE;
-      if (ok) {
-        const FfbInsRec& c = ins[cmp_i];
-        counter = c.op[1];
-        if (!starts_with_percent(counter)) ok = false;
-        if (ok && ffb_op_kind(c.op[2]) == FFB_OPK_BIGINT) { ok = false; status = FFB_E_CAPACITY; }
-        if (ok && ffb_op_kind(c.op[2]) != FFB_OPK_INT) ok = false;
-        if (ok) bound = ffb_op_int(c.op[2]);
-        rel = ffb_meta_cmp(c.meta);
-        if (rel == FFB_CMP_NONE) ok = false;
-        if (ok && ffb_meta_pred_neg(ins[latch].meta)) {
-          const uint32_t inv[7] = {0, FFB_CMP_GE, FFB_CMP_LT, FFB_CMP_GT, FFB_CMP_LE, FFB_CMP_NE, FFB_CMP_EQ};
-          rel = inv[rel];
-        }
-      }
-      int64_t stride = 0; bool have_stride = false;
-      if (ok) {
-        const uint64_t ch = ffb_op_hash(counter);
-        for (uint32_t b = 0; b < nb && ok; ++b) {
-          if (mark[b] != stamp) continue;
-          for (uint32_t i = block_start[b]; i < block_start[b + 1] && ok; ++i) {
-            const uint32_t m = FFB_META(i);
-            const uint32_t base = ffb_meta_base(m);
-            if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && ffb_meta_nops(m) == 3 &&
-                starts_with_percent(ins[i].op[0]) && ffb_op_hash(ins[i].op[0]) == ch &&
-                starts_with_percent(ins[i].op[1]) && ffb_op_hash(ins[i].op[1]) == ch) {
-              if (ffb_op_kind(ins[i].op[2]) == FFB_OPK_BIGINT) { ok = false; status = FFB_E_CAPACITY; break; }
-              if (ffb_op_kind(ins[i].op[2]) != FFB_OPK_INT) { ok = false; break; }
-              const int64_t imm = ffb_op_int(ins[i].op[2]);
-              if (have_stride) { ok = false; break; }
-              stride = base == FFB_BASE_SUB ? -imm : imm;
-              have_stride = true;
+    }
+    __syncwarp();
+    for (uint32_t b = lane; b < nb; b += 32) mark[b] = 0;
+    __syncwarp();
+    // ---- natural loops, one per header in ascending header order (cfg.py:124-151) ----
+    uint32_t n_loops = 0;
+    for (uint32_t h = 0; h < nb; ++h) {
+      const uint32_t stamp = h + 1;
+      int is_header = 0;
+      if (lane == 0) {
+        for (uint32_t p = pred_ptr[h]; p < pred_ptr[h + 1]; ++p) {
+          const uint32_t u = pred_list[p];
+          if (!dominates(idom, rpo_num, h, u)) continue;
+          is_header = 1;
+          mark[h] = stamp;                      // body = {h, u} + everything that reaches u without passing h
+          mark[u] = stamp;
+          uint32_t top = 0;
+          stack[top++] = u;
+          while (top) {
+            const uint32_t x = stack[--top];
+            if (x == h) continue;
+            for (uint32_t q = pred_ptr[x]; q < pred_ptr[x + 1]; ++q) {
+              const uint32_t y = pred_list[q];
+              if (mark[y] != stamp) { mark[y] = stamp; stack[top++] = y; }
             }
           }
         }
-        if (ok && (!have_stride || stride == 0)) ok = false;
       }
-      int64_t init = 0; bool have_init = false;
-      if (ok) {
-        const uint64_t ch = ffb_op_hash(counter);
-        // the LAST write before the header decides (cfg.py:246-254), so walk backwards and stop
-        for (int64_t i = (int64_t)h0 - 1; i >= 0; --i) {
-          const uint32_t m = FFB_META(i);
-          if (ffb_meta_nops(m) == 0 || !ffb_meta_dst_reg(m)) continue;      // the counter starts with '%'
-          const uint64_t d0 = ins[i].op[0];
-          if (!starts_with_percent(d0) || ffb_op_hash(d0) != ch) continue;
-          if (ffb_meta_base(m) == FFB_BASE_MOV && ffb_meta_nops(m) == 2) {
-            if (ffb_op_kind(ins[i].op[1]) == FFB_OPK_INT) { init = ffb_op_int(ins[i].op[1]); have_init = true; }
-            else if (ffb_op_kind(ins[i].op[1]) == FFB_OPK_BIGINT) status = FFB_E_CAPACITY;
+      is_header = __shfl_sync(kAll, is_header, 0);
+      if (!is_header) continue;
+      __syncwarp();
+      const uint32_t h0 = block_start[h];
+      // header label: the dictionary's last name that maps to the header's first instruction
+      int64_t best = -1;                        // (first-definition order << 32) | record index
+      for (uint32_t i = lane; i < L; i += 32) {
+        const uint32_t s = lt.find(lab[i].hash);
+        if (lt.last[s] != i || lab[i].index != h0) continue;       // only effective definitions
+        const int64_t cand = ((int64_t)lt.first[s] << 32) | (int64_t)i;
+        best = cand > best ? cand : best;
+      }
+      best = warp_max_i64(best);
+      const bool hl_any = best >= 0;
+      const uint64_t hl_hash = hl_any ? lab[(uint32_t)(best & 0xffffffff)].hash : 0;
+      const uint32_t hl_off = hl_any ? lab[(uint32_t)(best >> 32)].off : 0;
+      // ---- trip count ----
+      double trip = -1.0;
+      bool annotated = false;
+      if (hl_any) {
+        for (int q = 0; q < a.n_ann; ++q)
+          if (a.ann_hash[q] == hl_hash) { trip = a.ann_trip[q]; annotated = true; if (a.ann_hit && lane == 0) a.ann_hit[q] = 1; }
+      }
+      if (!annotated) {
+        // cfg.py:191-279; "last match in the body" = maximum index over the body's statements
+        bool ok = true;
+        int64_t latch = -1;
+        for (uint32_t b = 0; b < nb; ++b) {
+          if (mark[b] != stamp) continue;
+          for (uint32_t i = block_start[b] + lane; i < block_start[b + 1]; i += 32) {
+            const uint32_t m = FFB_META(i);
+            if (ffb_meta_cls(m) == FFB_CLS_BRANCH && ffb_meta_has_pred(m)) {
+              const uint32_t s = lt.find(ffb_op_hash(ins[i].aux));
+              if (lab[lt.last[s]].index == h0) latch = i;
+            }
           }
-          break;
         }
-        if (!have_init) ok = false;
+        latch = warp_max_i64(latch);
+        int64_t cmp_i = -1;
+        if (latch < 0) ok = false;
+        if (ok) {
+          const uint64_t preg = ins[latch].pred;
+          for (uint32_t b = 0; b < nb; ++b) {
+            if (mark[b] != stamp) continue;
+            for (uint32_t i = block_start[b] + lane; i < block_start[b + 1]; i += 32) {
+              const uint32_t m = FFB_META(i);
+              if (ffb_meta_base(m) == FFB_BASE_SETP && ffb_meta_nops(m) >= 1) {
+                const uint64_t d0 = ins[i].op[0];
+                if (ffb_op_kind(d0) != FFB_OPK_INT && ffb_op_hash(d0) == preg) cmp_i = i;
+              }
+            }
+          }
+          cmp_i = warp_max_i64(cmp_i);
+          if (cmp_i < 0 || ffb_meta_nops(FFB_META(cmp_i)) < 3) ok = false;
+        }
+        uint64_t counter = 0; int64_t bound = 0; uint32_t rel = FFB_CMP_NONE;
+        if (ok) {
+          const FfbInsRec& c = ins[cmp_i];
+          counter = c.op[1];
+          if (!starts_with_percent(counter)) ok = false;
+          if (ok && ffb_op_kind(c.op[2]) == FFB_OPK_BIGINT) { ok = false; status = FFB_E_CAPACITY; }
+          if (ok && ffb_op_kind(c.op[2]) != FFB_OPK_INT) ok = false;
+          if (ok) bound = ffb_op_int(c.op[2]);
+          rel = ffb_meta_cmp(c.meta);
+          if (rel == FFB_CMP_NONE) ok = false;
+          if (ok && ffb_meta_pred_neg(ins[latch].meta)) {
+            const uint32_t inv[7] = {0, FFB_CMP_GE, FFB_CMP_LT, FFB_CMP_GT, FFB_CMP_LE, FFB_CMP_NE, FFB_CMP_EQ};
+            rel = inv[rel];
+          }
+        }
+        int64_t stride = 0;
+        if (ok) {
+          // exactly one `add/sub counter, counter, <int literal>` in the body (cfg.py:229-240)
+          const uint64_t ch = ffb_op_hash(counter);
+          int n_upd = 0, n_bad = 0, n_big = 0;
+          int64_t my_stride = 0;
+          for (uint32_t b = 0; b < nb; ++b) {
+            if (mark[b] != stamp) continue;
+            for (uint32_t i = block_start[b] + lane; i < block_start[b + 1]; i += 32) {
+              const uint32_t m = FFB_META(i);
+              const uint32_t base = ffb_meta_base(m);
+              if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && ffb_meta_nops(m) == 3 && ffb_meta_dst_reg(m)) {
+                const FfbInsRec& r = ins[i];
+                if (ffb_op_hash(r.op[0]) == ch && starts_with_percent(r.op[1]) && ffb_op_hash(r.op[1]) == ch) {
+                  ++n_upd;
+                  if (ffb_op_kind(r.op[2]) == FFB_OPK_BIGINT) ++n_big;
+                  else if (ffb_op_kind(r.op[2]) != FFB_OPK_INT) ++n_bad;
+                  else my_stride = base == FFB_BASE_SUB ? -ffb_op_int(r.op[2]) : ffb_op_int(r.op[2]);
+                }
+              }
+            }
+          }
+          n_upd = warp_sum_i(n_upd); n_bad = warp_sum_i(n_bad); n_big = warp_sum_i(n_big);
+          if (n_big) status = FFB_E_CAPACITY;
+          if (n_upd != 1 || n_bad || n_big) ok = false;
+          else {
+            // the single matching lane holds the stride; others hold 0
+            stride = my_stride;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) stride += __shfl_xor_sync(kAll, stride, d);
+            if (stride == 0) ok = false;
+          }
+        }
+        int64_t init = 0;
+        if (ok) {
+          // the LAST write to the counter before the header decides (cfg.py:246-254)
+          const uint64_t ch = ffb_op_hash(counter);
+          int64_t found = -1;
+          for (int64_t hi = (int64_t)h0; hi > 0 && found < 0; hi -= 32) {
+            const int64_t i = hi - 1 - lane;                     // lane 0 looks at the latest statement
+            bool hit = false;
+            if (i >= 0) {
+              const uint32_t m = FFB_META(i);
+              if (ffb_meta_nops(m) != 0 && ffb_meta_dst_reg(m)) hit = ffb_op_hash(ins[i].op[0]) == ch;
+            }
+            const unsigned mask = __ballot_sync(kAll, hit);
+            if (mask) found = hi - 1 - (__ffs((int)mask) - 1);
+          }
+          bool have_init = false;
+          if (found >= 0) {
+            const FfbInsRec& r = ins[found];
+            if (ffb_meta_base(r.meta) == FFB_BASE_MOV && ffb_meta_nops(r.meta) == 2) {
+              if (ffb_op_kind(r.op[1]) == FFB_OPK_INT) { init = ffb_op_int(r.op[1]); have_init = true; }
+              else if (ffb_op_kind(r.op[1]) == FFB_OPK_BIGINT) status = FFB_E_CAPACITY;
+            }
+          }
+          if (!have_init) ok = false;
+        }
+        if (ok) {
+          // cfg.py:259-279, Python int arithmetic: "/" is true division, then ceil / floor
+          double trips = 0.0;
+          const double span_up = (double)(bound - init), span_dn = (double)(init - bound);
+          if (rel == FFB_CMP_LT && stride > 0) trips = ceil(span_up / (double)stride);
+          else if (rel == FFB_CMP_LE && stride > 0) trips = floor(span_up / (double)stride) + 1.0;
+          else if (rel == FFB_CMP_GT && stride < 0) trips = ceil(span_dn / (double)(-stride));
+          else if (rel == FFB_CMP_GE && stride < 0) trips = floor(span_dn / (double)(-stride)) + 1.0;
+          else if (rel == FFB_CMP_NE) {
+            const int64_t span = bound - init;
+            if (span % stride == 0 && span / stride > 0) trips = (double)(span / stride);
+            else ok = false;
+          } else ok = false;
+          if (ok) trip = trips < 1.0 ? 1.0 : trips;
+        }
+        if (!ok) trip = a.default_trip;
       }
-      if (ok) {
-        // cfg.py:259-279, Python int arithmetic: "/" is true division, then ceil / floor
-        double trips = 0.0;
-        const double span_up = (double)(bound - init), span_dn = (double)(init - bound);
-        if (rel == FFB_CMP_LT && stride > 0) trips = ceil(span_up / (double)stride);
-        else if (rel == FFB_CMP_LE && stride > 0) trips = floor(span_up / (double)stride) + 1.0;
-        else if (rel == FFB_CMP_GT && stride < 0) trips = ceil(span_dn / (double)(-stride));
-        else if (rel == FFB_CMP_GE && stride < 0) trips = floor(span_dn / (double)(-stride)) + 1.0;
-        else if (rel == FFB_CMP_NE) {
-          const int64_t span = bound - init;
-          if (span % stride == 0 && span / stride > 0) trips = (double)(span / stride);
-          else ok = false;
-        } else ok = false;
-        if (ok) trip = trips < 1.0 ? 1.0 : trips;
+      if (!(trip > 1.0)) trip = 1.0;                                  // cfg.py:181 max(1.0, trip)
+      int n_body = 0;
+      for (uint32_t b = lane; b < nb; b += 32)
+        if (mark[b] == stamp) { weight[b] *= trip; ++n_body; }       // cfg.py:52-53
+      n_body = warp_sum_i(n_body);
+      if (a.out_loops) {
+        if (lane == 0) {
+          FfbLoopRec lr;
+          lr.header = h; lr.n_body = (uint32_t)n_body; lr.trip = trip; lr.label_hash = hl_any ? hl_hash : 0;
+          lr.label_off = hl_off; lr.has_label = hl_any ? 1u : 0u;
+          a.out_loops[o1 + n_loops] = lr;
+        }
+        if (a.out_loop_body && (int64_t)(n_loops + 1) * nb <= a.loop_body_cap)
+          for (uint32_t b = lane; b < nb; b += 32) a.out_loop_body[(int64_t)n_loops * nb + b] = mark[b] == stamp ? 1 : 0;
       }
-      if (!ok) trip = a.default_trip;
+      ++n_loops;
+      __syncwarp();
     }
-    if (!(trip > 1.0)) trip = 1.0;                                  // cfg.py:181 max(1.0, trip)
-    uint32_t n_body = 0;
-    for (uint32_t b = 0; b < nb; ++b)
-      if (mark[b] == stamp) { weight[b] *= trip; ++n_body; }       // cfg.py:52-53
-    if (a.out_loops) {
-      FfbLoopRec lr;
-      lr.header = h; lr.n_body = n_body; lr.trip = trip; lr.label_hash = hl_any ? hl_hash : 0;
-      lr.label_off = hl_off; lr.has_label = hl_any ? 1u : 0u;
-      a.out_loops[o1 + n_loops] = lr;
-      if (a.out_loop_body && (int64_t)(n_loops + 1) * nb <= a.loop_body_cap)
-        for (uint32_t b = 0; b < nb; ++b) a.out_loop_body[(int64_t)n_loops * nb + b] = mark[b] == stamp ? 1 : 0;
-    }
-    ++n_loops;
-  }
-  // ---- one textual pass: affine scales, aligned fraction, dynamic counts ----
-  st.clear();
-  double n_mem = 0.0, mem_bytes = 0.0, u_fp = 0.0, u_int = 0.0, u_sfu = 0.0, u_alu = 0.0, n_sync = 0.0;
-  double al_hit = 0.0, al_tot = 0.0;
-  for (uint32_t i = 0; i < n; ++i) {
-    if (i + 6 < n) FFB_PREFETCH(&ins[i + 6]);
-    const FfbInsRec r = ins[i];
-    const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m), base = ffb_meta_base(m);
-    const double wgt = weight[block_of[i]];
-    const bool is_mem = cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE;
-    if (is_mem) {
-      const uint32_t space = ffb_meta_space(m), bytes = ffb_meta_bytes(m);
-      if (space != FFB_SP_PARAM) { n_mem += wgt; mem_bytes += wgt * (double)bytes; }      // features.py:72-75
-      if (space == FFB_SP_GLOBAL) {                                                      // alignment.py:137-144
-        int64_t sc = kNoneScale;
-        const uint32_t ak = ffb_meta_addr(m);
-        if (ak == FFB_ADDR_SYMBOL) sc = 0;
-        else if (ak == FFB_ADDR_REG) sc = st.get(ffb_op_hash(r.aux));
-        al_tot += wgt;
-        if (sc_known(sc) && sc != kBigScale && (sc < 0 ? -sc : sc) == (int64_t)bytes) al_hit += wgt;
+    __syncwarp();
+    // ---- one textual pass: affine scales, aligned fraction, dynamic counts ----
+    double n_mem = 0.0, mem_bytes = 0.0, u_fp = 0.0, u_int = 0.0, u_sfu = 0.0, u_alu = 0.0, n_sync = 0.0;
+    double al_hit = 0.0, al_tot = 0.0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+      const uint32_t cnt = n - c0 < 32 ? n - c0 : 32;
+      if ((uint32_t)lane < cnt) {
+        const uint4* src = reinterpret_cast<const uint4*>(ins + c0 + lane);
+        uint4* dst = reinterpret_cast<uint4*>(stage + lane);
+        dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
+        wstage[lane] = weight[block_of[c0 + lane]];
       }
-      if (cls == FFB_CLS_MEMLOAD && nops >= 1 && ffb_meta_dst_reg(m))                    // alignment.py:84-88
-        st.put(ffb_op_hash(r.op[0]), space == FFB_SP_PARAM ? 0 : kNoneScale);
-      continue;
-    }
-    if (cls == FFB_CLS_FP32) u_fp += wgt;
-    else if (cls == FFB_CLS_INT) u_int += wgt;
-    else if (cls == FFB_CLS_SFU) u_sfu += wgt;
-    else if (cls == FFB_CLS_ALU) u_alu += wgt;
-    else if (cls == FFB_CLS_SYNC) n_sync += wgt;
-    if (nops == 0 || !ffb_meta_dst_reg(m)) continue;                                      // alignment.py:91-95
-    const uint64_t dst = ffb_op_hash(r.op[0]);
-    int64_t v;
-    if (base == FFB_BASE_MOV && nops == 2) v = operand_scale(r.op[1], st);
-    else if ((base == FFB_BASE_CVT || base == FFB_BASE_CVTA) && nops >= 2) {
-      // scale of the LAST operand
-      uint64_t lastd = nops == 2 ? r.op[1] : nops == 3 ? r.op[2] : nops == 4 ? r.op[3] : r.aux;
-      if (nops > 5) { status = FFB_E_CAPACITY; lastd = 0; }
-      v = operand_scale(lastd, st);
-    } else if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && nops == 3) {
-      const int64_t x = operand_scale(r.op[1], st), y = operand_scale(r.op[2], st);
-      v = base == FFB_BASE_ADD ? sc_add(x, y) : sc_add(x, sc_neg(y));
-    } else if (base == FFB_BASE_MUL && nops == 3) v = mul_scale(r.op[1], r.op[2], st);
-    else if ((base == FFB_BASE_MAD || base == FFB_BASE_FMA) && nops == 4) v = sc_add(mul_scale(r.op[1], r.op[2], st), operand_scale(r.op[3], st));
-    else if (base == FFB_BASE_SHL && nops == 3) {
-      const int64_t x = operand_scale(r.op[1], st);
-      if (!sc_known(x) || !is_int_lit(r.op[2])) v = kNoneScale;
-      else {
-        const int64_t sh = int_as_scale(r.op[2]);
-        if (sh == kBigScale || sh < 0) { status = FFB_E_CAPACITY; v = kNoneScale; }   // 1 << huge / negative: reference raises
-        else v = x == 0 ? 0 : (sh >= 61 ? kBigScale : sc_mul(x, (int64_t)1 << sh));
+      __syncwarp();
+      if (lane == 0) {
+        for (uint32_t q0 = 0; q0 < cnt; ++q0) {
+          const FfbInsRec& r = stage[q0];
+          const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m), base = ffb_meta_base(m);
+          const double wgt = wstage[q0];
+          const bool is_mem = cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE;
+          if (is_mem) {
+            const uint32_t space = ffb_meta_space(m), bytes = ffb_meta_bytes(m);
+            if (space != FFB_SP_PARAM) { n_mem += wgt; mem_bytes += wgt * (double)bytes; }      // features.py:72-75
+            if (space == FFB_SP_GLOBAL) {                                                      // alignment.py:137-144
+              int64_t sc = kNoneScale;
+              const uint32_t ak = ffb_meta_addr(m);
+              if (ak == FFB_ADDR_SYMBOL) sc = 0;
+              else if (ak == FFB_ADDR_REG) sc = st.get(ffb_op_hash(r.aux));
+              al_tot += wgt;
+              if (sc_known(sc) && sc != kBigScale && (sc < 0 ? -sc : sc) == (int64_t)bytes) al_hit += wgt;
+            }
+            if (cls == FFB_CLS_MEMLOAD && nops >= 1 && ffb_meta_dst_reg(m))                    // alignment.py:84-88
+              st.put(ffb_op_hash(r.op[0]), space == FFB_SP_PARAM ? 0 : kNoneScale);
+            continue;
+          }
+          if (cls == FFB_CLS_FP32) u_fp += wgt;
+          else if (cls == FFB_CLS_INT) u_int += wgt;
+          else if (cls == FFB_CLS_SFU) u_sfu += wgt;
+          else if (cls == FFB_CLS_ALU) u_alu += wgt;
+          else if (cls == FFB_CLS_SYNC) n_sync += wgt;
+          if (nops == 0 || !ffb_meta_dst_reg(m)) continue;                                      // alignment.py:91-95
+          const uint64_t dst = ffb_op_hash(r.op[0]);
+          int64_t v;
+          if (base == FFB_BASE_MOV && nops == 2) v = operand_scale_c(r.op[1], st);
+          else if ((base == FFB_BASE_CVT || base == FFB_BASE_CVTA) && nops >= 2) {
+            uint64_t lastd = nops == 2 ? r.op[1] : nops == 3 ? r.op[2] : nops == 4 ? r.op[3] : r.aux;   // LAST operand
+            if (nops > 5) { status = FFB_E_CAPACITY; lastd = 0; }
+            v = operand_scale_c(lastd, st);
+          } else if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && nops == 3) {
+            const int64_t x = operand_scale_c(r.op[1], st), y = operand_scale_c(r.op[2], st);
+            v = base == FFB_BASE_ADD ? sc_add(x, y) : sc_add(x, sc_neg(y));
+          } else if (base == FFB_BASE_MUL && nops == 3) v = mul_scale_c(r.op[1], r.op[2], st);
+          else if ((base == FFB_BASE_MAD || base == FFB_BASE_FMA) && nops == 4)
+            v = sc_add(mul_scale_c(r.op[1], r.op[2], st), operand_scale_c(r.op[3], st));
+          else if (base == FFB_BASE_SHL && nops == 3) {
+            const int64_t x = operand_scale_c(r.op[1], st);
+            if (!sc_known(x) || !is_int_lit(r.op[2])) v = kNoneScale;
+            else {
+              const int64_t sh = int_as_scale(r.op[2]);
+              if (sh == kBigScale || sh < 0) { status = FFB_E_CAPACITY; v = kNoneScale; }   // 1 << huge / negative: reference raises
+              else v = x == 0 ? 0 : (sh >= 61 ? kBigScale : sc_mul(x, (int64_t)1 << sh));
+            }
+          } else if (base == FFB_BASE_SETP) continue;
+          else {
+            // unmodelled producer: uniform only if it has sources and all of them are uniform
+            bool all0 = nops >= 2;
+            for (uint32_t q = 1; q < nops && q < 4 && all0; ++q) all0 = operand_scale_c(r.op[q], st) == 0;
+            if (all0 && nops >= 5) all0 = operand_scale_c(r.aux, st) == 0;
+            if (all0 && nops >= 6 && ffb_meta_extra_reg(m)) { status = FFB_E_CAPACITY; all0 = false; }
+            v = all0 ? 0 : kNoneScale;
+          }
+          st.put(dst, v);
+        }
       }
-    } else if (base == FFB_BASE_SETP) continue;
-    else {
-      // unmodelled producer: uniform only if it has sources and all of them are uniform
-      bool all0 = nops >= 2;
-      for (uint32_t q = 1; q < nops && q < 4 && all0; ++q) all0 = operand_scale(r.op[q], st) == 0;
-      if (all0 && nops >= 5) all0 = operand_scale(r.aux, st) == 0;
-      if (all0 && nops >= 6 && ffb_meta_extra_reg(m)) { status = FFB_E_CAPACITY; all0 = false; }
-      v = all0 ? 0 : kNoneScale;
+      __syncwarp();
     }
-    st.put(dst, v);
-  }
-  feat[FFB_F_N_MEM] = n_mem; feat[FFB_F_MEM_BYTES] = mem_bytes;
-  feat[FFB_F_FP32] = u_fp; feat[FFB_F_INT] = u_int; feat[FFB_F_SFU] = u_sfu; feat[FFB_F_ALU] = u_alu;
-  feat[FFB_F_N_SYNC] = n_sync;
-  feat[FFB_F_ALIGNED] = al_tot == 0.0 ? 1.0 : al_hit / al_tot;                            // alignment.py:145-147
-  feat[FFB_F_STATIC_SHARED] = (double)inf.static_shared;
-  feat[FFB_F_REGS_DECLARED] = (double)inf.regs_declared;
-  feat[FFB_F_N_INSTR] = (double)n;
-  a.status[k] = status;
-  fi.n_blocks = nb; fi.n_edges = n_edges; fi.n_loops = n_loops;
-  if (a.flow) a.flow[k] = fi;
-  if (a.out_block_start) for (uint32_t b = 0; b <= nb; ++b) a.out_block_start[o1 + b] = block_start[b];
-  if (a.out_weights) for (uint32_t b = 0; b < nb; ++b) a.out_weights[o1 + b] = weight[b];
-  if (a.out_edges) {
-    uint32_t e = 0;
-    for (uint32_t b = 0; b < nb; ++b) {
-      if (succ0[b] >= 0) { a.out_edges[2 * (2 * o1 + e)] = (int32_t)b; a.out_edges[2 * (2 * o1 + e) + 1] = succ0[b]; ++e; }
-      if (succ1[b] >= 0) { a.out_edges[2 * (2 * o1 + e)] = (int32_t)b; a.out_edges[2 * (2 * o1 + e) + 1] = succ1[b]; ++e; }
+    status = __shfl_sync(kAll, status, 0) | status;      // lane 0 owns the dataflow errors; trip errors are uniform
+    if (lane == 0) {
+      feat[FFB_F_N_MEM] = n_mem; feat[FFB_F_MEM_BYTES] = mem_bytes;
+      feat[FFB_F_FP32] = u_fp; feat[FFB_F_INT] = u_int; feat[FFB_F_SFU] = u_sfu; feat[FFB_F_ALU] = u_alu;
+      feat[FFB_F_N_SYNC] = n_sync;
+      feat[FFB_F_ALIGNED] = al_tot == 0.0 ? 1.0 : al_hit / al_tot;                            // alignment.py:145-147
+      feat[FFB_F_STATIC_SHARED] = (double)inf.static_shared;
+      feat[FFB_F_REGS_DECLARED] = (double)inf.regs_declared;
+      feat[FFB_F_N_INSTR] = (double)n;
+      a.status[k] = status;
+      fi.n_blocks = nb; fi.n_edges = n_edges; fi.n_loops = n_loops;
+      if (a.flow) a.flow[k] = fi;
     }
+    if (a.out_block_start) for (uint32_t b = lane; b <= nb; b += 32) a.out_block_start[o1 + b] = block_start[b];
+    if (a.out_weights) for (uint32_t b = lane; b < nb; b += 32) a.out_weights[o1 + b] = weight[b];
+    if (a.out_edges && lane == 0) {
+      uint32_t e = 0;
+      for (uint32_t b = 0; b < nb; ++b) {
+        if (succ0[b] >= 0) { a.out_edges[2 * (2 * o1 + e)] = (int32_t)b; a.out_edges[2 * (2 * o1 + e) + 1] = succ0[b]; ++e; }
+        if (succ1[b] >= 0) { a.out_edges[2 * (2 * o1 + e)] = (int32_t)b; a.out_edges[2 * (2 * o1 + e) + 1] = succ1[b]; ++e; }
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -576,7 +736,8 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
                o_pp = take(n1, 4), o_pl = take(2 * n1, 4), o_rn = take(n1, 4), o_ro = take(n1, 4), o_id = take(n1, 4),
                o_mk = take(n1, 4), o_sk = take(n1, 4), o_w = take(n1, 8), o_lk = take(nL, 8), o_lf = take(nL, 4),
                o_ll = take(nL, 4), o_sk2 = take(nS, 8), o_sv = take(nS, 8),
-               o_ah = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8), o_at = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8);
+               o_ah = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8), o_at = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8),
+               o_work = take(2, 8);
   int32_t rc = ffb_reserve(ctx, &ctx->d_flow, bytes);
   if (rc) return rc;
   char* base = (char*)ctx->d_flow.p;
@@ -595,6 +756,8 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   a.lab_key = (uint64_t*)(base + o_lk); a.lab_first = (uint32_t*)(base + o_lf); a.lab_last = (uint32_t*)(base + o_ll);
   a.sc_key = (uint64_t*)(base + o_sk2); a.sc_val = (int64_t*)(base + o_sv);
   a.ann_hash = (const uint64_t*)(base + o_ah); a.ann_trip = (const double*)(base + o_at);
+  a.work = (unsigned long long*)(base + o_work);
+  FFB_CUDA(ctx, cudaMemsetAsync(a.work, 0, 8, stream));
   if (a.n_ann > 0) {
     if (!d->h_ann_hash || !d->h_ann_trip) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_kernel_features: annotation arrays missing");
     rc = ffb_stage_reserve(ctx, (size_t)a.n_ann * 16);
@@ -608,8 +771,10 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   }
   a.out_block_start = d->d_block_start; a.out_edges = d->d_edges; a.out_loops = d->d_loops;
   a.out_loop_body = d->d_loop_body; a.loop_body_cap = d->loop_body_cap; a.out_weights = d->d_weights;
-  const int64_t ctas = (K + kFlowThreads - 1) / kFlowThreads;
-  FFB_LAUNCH(flow_kernel, (unsigned)ctas, kFlowThreads, 0, stream, a);
+  int64_t ctas = (K + kFlowWarps - 1) / kFlowWarps;
+  const int64_t max_ctas = (int64_t)ctx->sm_count * 16;
+  if (ctas > max_ctas) ctas = max_ctas;
+  FFB_LAUNCH(flow_kernel, (unsigned)ctas, kFlowWarps * 32, 0, stream, a);
   return ffb_check_launch(ctx, "flow_kernel");
 }
 

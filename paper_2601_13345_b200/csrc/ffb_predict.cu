@@ -333,13 +333,13 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   double* h = (double*)ctx->h_stage;
   double* h_spec = h;
   double* h_sd = h_spec + n_spec;
-  double* h_log = h_sd + n_sd;
+  double* h_ctab = h_sd + n_sd;            // 64*S doubles precede it: rows stay 32-byte aligned
+  double* h_log = h_ctab + 4 * n_sc;
   double* h_cap = h_log + n_log;
   double* h_scale = h_cap + n_cap;
   double* h_fadj = h_scale + n_sc;
   double* h_ok = h_fadj + n_sc;
-  double* h_ctab = h_ok + n_sc;
-  double* h_psm = h_ctab + 4 * n_sc;
+  double* h_psm = h_ok + n_sc;
   int32_t* h_shape = (int32_t*)(h_psm + n_psm);
   memcpy(h_spec, g->h_spec, n_spec * sizeof(double));
   memcpy(h_cap, g->h_cap, n_cap * sizeof(double));
@@ -380,13 +380,13 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   double* d = (double*)ctx->d_tables.p;
   tb.spec = d;
   tb.sd = tb.spec + n_spec;
-  tb.shape_log = tb.sd + n_sd;
+  tb.cap_tab = tb.sd + n_sd;
+  tb.shape_log = tb.cap_tab + 4 * n_sc;
   tb.cap = tb.shape_log + n_log;
   tb.cap_scale = tb.cap + n_cap;
   tb.cap_fadj = tb.cap_scale + n_sc;
   tb.cap_ok = tb.cap_fadj + n_sc;
-  tb.cap_tab = tb.cap_ok + n_sc;
-  tb.psm = tb.cap_tab + 4 * n_sc;
+  tb.psm = tb.cap_ok + n_sc;
   tb.shape = (const int32_t*)(tb.psm + n_psm);
   tb.psm_n = psm_n;
 
