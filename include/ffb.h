@@ -218,6 +218,10 @@ typedef struct {
    * n_instr / n_labels a previous histogram-only call returned)                              */
   const int64_t* d_ins_base;  /* [K] */
   const int64_t* d_lab_base;  /* [K] */
+  const int64_t* d_ins_cap;   /* optional [K]: record slots available per segment.  With caps the bases
+                                 need not come from a counting pass (single-pass mode, e.g. bytes/12
+                                 slots); a segment that needs more gets status FFB_E_CAPACITY */
+  const int64_t* d_lab_cap;   /* optional [K] */
   void* d_ins;                /* FfbInsRecC[sum n_instr]                                        */
   void* d_labels;             /* FfbLabelRecC[sum n_labels]                                     */
   uint32_t* d_meta;           /* optional [sum n_instr]: copy of FfbInsRecC.meta, 4 B per instruction

@@ -62,6 +62,8 @@ struct LexArgs {
   // record mode
   const int64_t* ins_base;
   const int64_t* lab_base;
+  const int64_t* ins_cap;     // optional per-segment record capacities (single-pass mode)
+  const int64_t* lab_cap;
   FfbInsRec* ins;
   FfbLabelRec* labels;
   uint32_t* meta;             // optional compact copy of the meta words
@@ -301,6 +303,11 @@ FFB_D OpcodeInfo classify_opcode(const TokTable& tt, const uint8_t* s, int o0, i
 FFB_D uint64_t norm_hash(const uint8_t* s, int a, int b) {
   uint64_t h = kFnvBasis;
   int i = a;
+  for (; i < b; ++i) {                          // common case: no blank inside the operand
+    const unsigned c = s[i];
+    if (ffb_is_ws(c)) break;
+    h = ffb_hash_step(h, c);
+  }
   while (i < b) {
     const unsigned c = s[i];
     if (!ffb_is_ws(c)) { h = ffb_hash_step(h, c); ++i; continue; }
@@ -509,6 +516,7 @@ struct Emit {
   int64_t seg_begin;      // global offset of the segment
   int64_t abase;          // global offset of smem index 0
   int64_t ins_at, lab_at; // next global record slots
+  int64_t ins_limit, lab_limit;   // first slot NOT owned by this segment
   int dcl_at;
   uint32_t line;          // source line of the current line
   uint32_t cnt[FFB_N_CLASSES];
@@ -571,11 +579,14 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
     sp->opc_off = (uint32_t)(em.abase + o0 - em.seg_begin);
     sp->opc_len = (uint32_t)(o1 - o0);
   }
-  // operands: split at depth-0 commas (ptx.py:144-162)
+  // operands: split at depth-0 commas (ptx.py:144-162).  Phase 1 only records the spans, so that
+  // the per-operand work below starts at the same instruction for every lane of the warp
+  // (describing operands inside this byte loop would run one lane at a time).
   int depth = 0, ps = -1, pe = -1, count = 0, last_s = -1, last_e = -1;
-  uint32_t addr_kind = FFB_ADDR_ABSENT;
-  bool dst_reg = false, extra_reg = false;
+  int s0 = 0, e0 = 0, s1 = 0, e1 = 0, s2 = 0, e2 = 0, s3 = 0, e3 = 0, s4 = 0, e4 = 0, as = -1, ae = -1;
+  bool extra_reg = false;
   const bool is_mem = oc.cls == FFB_CLS_MEMLOAD || oc.cls == FFB_CLS_MEMSTORE;
+  const bool aux_is_op4 = !is_mem && oc.cls != FFB_CLS_BRANCH;
   for (int q = o1; q <= e; ++q) {
     const unsigned c = q < e ? s[q] : 0u;
     if (q < e) {
@@ -584,12 +595,11 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
     }
     if (q == e || (c == ',' && depth == 0)) {
       if (ps >= 0) {
-        if (count < 4) rec.op[count] = describe_operand(s, ps, pe);
-        else if (count == 4 && !is_mem && oc.cls != FFB_CLS_BRANCH) rec.aux = describe_operand(s, ps, pe);
-        else if (count >= 5 && s[ps] == '%') extra_reg = true;
-        if (count == 4 && (is_mem || oc.cls == FFB_CLS_BRANCH) && s[ps] == '%') extra_reg = true;
-        if (count == 0) dst_reg = s[ps] == '%';
-        if (is_mem && addr_kind == FFB_ADDR_ABSENT && s[ps] == '[') addr_kind = describe_address(s, ps, pe, &rec.aux);
+        if (count == 0) { s0 = ps; e0 = pe; } else if (count == 1) { s1 = ps; e1 = pe; }
+        else if (count == 2) { s2 = ps; e2 = pe; } else if (count == 3) { s3 = ps; e3 = pe; }
+        else if (count == 4) { s4 = ps; e4 = pe; if (!aux_is_op4 && s[ps] == '%') extra_reg = true; }
+        else if (s[ps] == '%') extra_reg = true;
+        if (is_mem && as < 0 && s[ps] == '[') { as = ps; ae = pe; }
         if (sp && count < FFB_MAX_SPAN_OPS) {
           sp->op_off[count] = (uint32_t)(em.abase + ps - em.seg_begin);
           sp->op_len[count] = (uint32_t)(pe - ps);
@@ -603,13 +613,24 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
       pe = q + 1;
     }
   }
-  if (oc.cls == FFB_CLS_BRANCH) rec.aux = last_s >= 0 ? ffb_op_make(FFB_OPK_REG, norm_hash(s, last_s, last_e)) : 0ull;
+  // Phase 2: describe the operands, slot by slot
+  const bool dst_reg = count > 0 && s[s0] == '%';
+  if (count > 0) rec.op[0] = describe_operand(s, s0, e0);
+  if (count > 1) rec.op[1] = describe_operand(s, s1, e1);
+  if (count > 2) rec.op[2] = describe_operand(s, s2, e2);
+  if (count > 3) rec.op[3] = describe_operand(s, s3, e3);
+  uint32_t addr_kind = FFB_ADDR_ABSENT;
+  if (aux_is_op4) { if (count > 4) rec.aux = describe_operand(s, s4, e4); }
+  else if (is_mem) { if (as >= 0) addr_kind = describe_address(s, as, ae, &rec.aux); }
+  else rec.aux = last_s >= 0 ? ffb_op_make(FFB_OPK_REG, norm_hash(s, last_s, last_e)) : 0ull;
   if (sp) sp->n_ops = (uint32_t)count;
   rec.meta = oc.cls | (oc.space << 4) | ((oc.bytes & 63u) << 7) | (oc.base << 13) | ((has_pred ? 1u : 0u) << 18) |
              ((neg ? 1u : 0u) << 19) | ((uint32_t)(count > 7 ? 7 : count) << 20) | (oc.cmp << 23) | (addr_kind << 26) |
              ((dst_reg ? 1u : 0u) << 28) | ((extra_reg ? 1u : 0u) << 29);
-  em.a->ins[em.ins_at] = rec;
-  if (em.a->meta) em.a->meta[em.ins_at] = rec.meta;
+  if (em.ins_at < em.ins_limit) {
+    em.a->ins[em.ins_at] = rec;
+    if (em.a->meta) em.a->meta[em.ins_at] = rec.meta;
+  }
   em.ins_at += 1;
 }
 
@@ -668,7 +689,7 @@ FFB_D LineSummary walk_line(const uint8_t* s, int b, int e, bool pending_in, int
             const uint64_t h0 = norm_hash(s, pos, k);
             L.hash = h0; L.index = (uint32_t)(em.ins_at - em.a->ins_base[em.seg]);
             L.off = (uint32_t)(em.abase + pos - em.seg_begin);
-            em.a->labels[em.lab_at] = L;
+            if (em.lab_at < em.lab_limit) em.a->labels[em.lab_at] = L;
           }
           em.lab_at += 1;
         }
@@ -778,6 +799,8 @@ lex_corpus_kernel(LexArgs a) {
     em.tok.key = s_tok_key; em.tok.val = s_tok_val;
     em.ins_at = kRecords ? a.ins_base[seg] : 0;
     em.lab_at = kRecords ? a.lab_base[seg] : 0;
+    em.ins_limit = (kRecords && a.ins_cap) ? em.ins_at + a.ins_cap[seg] : 0x7fffffffffffffffLL;
+    em.lab_limit = (kRecords && a.lab_cap) ? em.lab_at + a.lab_cap[seg] : 0x7fffffffffffffffLL;
     em.dcl_at = 0;
 #pragma unroll
     for (int c = 0; c < FFB_N_CLASSES; ++c) em.cnt[c] = 0;
@@ -1024,7 +1047,7 @@ lex_corpus_kernel(LexArgs a) {
                     FfbLabelRec L;
                     L.hash = norm_hash(s, fb, lb); L.index = (uint32_t)(em.ins_at - a.ins_base[seg]);
                     L.off = (uint32_t)(abase + fb - seg_begin);
-                    a.labels[em.lab_at] = L;
+                    if (em.lab_at < em.lab_limit) a.labels[em.lab_at] = L;
                   }
                 }
               }
@@ -1086,6 +1109,8 @@ lex_corpus_kernel(LexArgs a) {
       else if (pending) status = FFB_E_MALFORMED_PTX;                                  // :272-273
       else if (n_instr == 0) status = FFB_E_MALFORMED_PTX;                             // :274-275
     }
+    if (kRecords && status == FFB_OK && ((a.ins_cap && (int64_t)n_instr > a.ins_cap[seg]) || (a.lab_cap && (int64_t)n_labels > a.lab_cap[seg])))
+      status = FFB_E_CAPACITY;            // single-pass mode: the segment outgrew its record slots
     uint32_t tot[FFB_N_CLASSES];
 #pragma unroll
     for (int c = 0; c < FFB_N_CLASSES; ++c) tot[c] = (uint32_t)warp_sum_u64(em.cnt[c]);
@@ -1151,7 +1176,7 @@ extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* st
   a.text = d->d_text; a.n_bytes = d->n_bytes; a.seg_off = d->d_seg_off; a.n_segs = d->n_segs;
   a.order = d->d_order; a.work = (unsigned long long*)ctx->d_lex.p;
   a.hist = d->d_hist; a.info = d->d_info;
-  a.ins_base = d->d_ins_base; a.lab_base = d->d_lab_base;
+  a.ins_base = d->d_ins_base; a.lab_base = d->d_lab_base; a.ins_cap = d->d_ins_cap; a.lab_cap = d->d_lab_cap;
   a.ins = (FfbInsRec*)d->d_ins; a.labels = (FfbLabelRec*)d->d_labels;
   a.spans = d->d_spans; a.decls = d->d_decls; a.meta = d->d_meta;
   a.want_name = nullptr; a.want_len = 0;

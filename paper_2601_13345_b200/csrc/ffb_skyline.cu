@@ -24,7 +24,7 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kBuckets = 256;
 constexpr uint32_t kPad = 0xffffffffu;
 
@@ -49,6 +49,7 @@ struct SkyArgs {
   int resident;             // points staged in shared memory
   int surv_cap;             // survivor capacity (entries of s_pm / s_gs)
   int sort_cap;             // power of two >= surv_cap (entries of s_idx)
+  int tie_smem;             // tie ranks staged in shared memory as u16
   // per-group outputs (optional)
   uint32_t* front_idx;
   uint32_t* front_n;
@@ -141,6 +142,7 @@ skyline_group_kernel(SkyArgs a) {
   double* s_pm = s_t + (a.resident ? a.group_size : 0);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_pm + MC);
   uint32_t* s_gs = s_idx + a.sort_cap;
+  uint16_t* s_tie = reinterpret_cast<uint16_t*>(s_gs + MC);
 
   const double* ge = a.e + p0;
   const double* gt = a.t + p0;
@@ -152,6 +154,7 @@ skyline_group_kernel(SkyArgs a) {
   for (int i = tid; i < G; i += kThreads) {
     const double tv = gt[i];
     if (a.resident) { s_e[i] = ge[i]; s_t[i] = tv; }
+    if (a.tie_smem) s_tie[i] = (uint16_t)a.tie[i];
     tmin = tv < tmin ? tv : tmin;
   }
   const double t_peak = block_reduce_min(tmin, s_part);
@@ -181,9 +184,9 @@ skyline_group_kernel(SkyArgs a) {
     }
   }
   __syncthreads();
-  // exclusive prefix-min over buckets (kThreads == kBuckets)
+  // exclusive prefix-min over buckets (threads beyond kBuckets carry the identity)
   {
-    unsigned long long v = s_bmin[tid];
+    unsigned long long v = tid < kBuckets ? s_bmin[tid] : ~0ull;
     unsigned long long incl = v;
     const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -201,7 +204,7 @@ skyline_group_kernel(SkyArgs a) {
     if (lane == 0) excl = ~0ull;
     excl = before < excl ? before : excl;
     __syncthreads();
-    s_bmin[tid] = excl;
+    if (tid < kBuckets) s_bmin[tid] = excl;
   }
   __syncthreads();
   // ---- 4. cull, collect survivors ----
@@ -243,6 +246,7 @@ skyline_group_kernel(SkyArgs a) {
 
   // ---- 5. bitonic sort of survivors by (e, t, tie) ----
   auto tie_of = [&](uint32_t i) -> uint64_t {
+    if (a.tie_smem) return s_tie[i];
     if (a.tie) return a.tie[i];
     if (a.id) return a.id[p0 + i];
     return (uint64_t)i;
@@ -258,13 +262,12 @@ skyline_group_kernel(SkyArgs a) {
   };
   for (int k = 2; k <= m2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < m2; i += kThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint32_t x = s_idx[i], y = s_idx[ixj];
-          const bool asc = (i & k) == 0;
-          if (less(y, x) == asc) { s_idx[i] = y; s_idx[ixj] = x; }
-        }
+      for (int p = tid; p < (m2 >> 1); p += kThreads) {      // one compare-exchange per pair
+        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+        const int ixj = i | j;
+        const uint32_t x = s_idx[i], y = s_idx[ixj];
+        const bool asc = (i & k) == 0;
+        if (less(y, x) == asc) { s_idx[i] = y; s_idx[ixj] = x; }
       }
       __syncthreads();
     }
@@ -326,12 +329,12 @@ skyline_group_kernel(SkyArgs a) {
   }
 }
 
-struct Plan { int resident; int surv_cap; int sort_cap; size_t smem; };
+struct Plan { int resident; int surv_cap; int sort_cap; int tie_smem; size_t smem; };
 
 // Survivor capacity = group size whenever shared memory allows, so a front made of ties
 // (every candidate on it) is still exact; two CTAs per SM stay resident for the 3248-point
 // groups of the headline workload (52 KB of points + 55 KB of survivor arrays).
-Plan plan_groups(const FfbContext* ctx, int64_t group_size) {
+Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie) {
   Plan p;
   const size_t limit = ctx->smem_optin ? ctx->smem_optin - 4096 : 96 * 1024;
   auto need = [](int64_t mc, bool resident, int64_t g) {
@@ -344,14 +347,20 @@ Plan plan_groups(const FfbContext* ctx, int64_t group_size) {
   int64_t sc = 32; while (sc < mc) sc <<= 1;
   p.surv_cap = (int)mc; p.sort_cap = (int)sc;
   p.smem = need(mc, p.resident != 0, group_size);
+  p.tie_smem = 0;
+  if (has_tie && p.resident && group_size <= 65535 && p.smem + (size_t)group_size * 2 + 16 <= limit) {
+    p.tie_smem = 1;
+    p.smem += (size_t)group_size * 2 + 16;
+  }
   return p;
 }
 
 int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t stream) {
-  Plan p = plan_groups(ctx, a.group_size);
+  Plan p = plan_groups(ctx, a.group_size, a.tie != nullptr);
   a.resident = p.resident;
   a.surv_cap = p.surv_cap;
   a.sort_cap = p.sort_cap;
+  a.tie_smem = p.tie_smem;
   if (n_groups > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "skyline: too many groups for one launch");
   FFB_CUDA(ctx, cudaFuncSetAttribute(skyline_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   FFB_LAUNCH(skyline_group_kernel, (unsigned)n_groups, kThreads, p.smem, stream, a);

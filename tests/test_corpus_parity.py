@@ -78,3 +78,21 @@ def test_line_longer_than_tile_is_reported(backend):
     src = ".entry a()\n{\n add.s32 %r1, %r1, " + "1" * 6000 + ";\n ret;\n}\n"
     res = corpus.lex_histogram(_corpus([src]))
     assert int(res.info_np()[0]["status"]) == 11       # FFB_E_CAPACITY, never a silent wrong answer
+
+
+def test_single_pass_records_equal_two_pass(backend):
+    """Single-pass record mode (capacity slots) gives the same histograms and feature rows as the
+    counting + record passes, and reports segments that outgrow their slots."""
+    n = 10 if backend == "emul" else 400
+    text, offs = synth.ptx_corpus(seed=13, n_kernels=n, lo=20, hi=500 if backend == "emul" else 3000)
+    dense = ".entry d()\n{\n" + "ret;\n" * 300 + "}\n"          # 5-byte statements: needs more slots than len/12
+    blob = text + dense.encode()
+    offs = np.concatenate([offs, [len(blob)]])
+    corp = corpus.upload_corpus(blob, offs)
+    lex2, fl2 = corpus.analyze_corpus(corp)
+    lex1 = corpus.lex_records_single_pass(corp)
+    fl1 = corpus.kernel_features(corp, lex1)
+    st1, st2 = fl1.status.cpu().numpy(), fl2.status.cpu().numpy()
+    assert (st2 == 0).all() and (st1[:-1] == 0).all() and st1[-1] == 11
+    assert np.array_equal(lex1.hist.cpu().numpy(), lex2.hist.cpu().numpy())
+    assert fl1.feat.cpu().numpy()[:-1, :11].tobytes() == fl2.feat.cpu().numpy()[:-1, :11].tobytes()
