@@ -519,7 +519,7 @@ struct Emit {
   int64_t ins_limit, lab_limit;   // first slot NOT owned by this segment
   int dcl_at;
   uint32_t line;          // source line of the current line
-  uint32_t cnt[FFB_N_CLASSES];
+  uint64_t c0, c1, c2;    // nine 21-bit class counters, three per word (no dynamically indexed array)
   unsigned long long shared_bytes, regs;
 };
 
@@ -562,7 +562,10 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
   int o1 = o0;
   while (o1 < e && !ffb_is_ws(s[o1])) ++o1;
   const OpcodeInfo oc = classify_opcode(em.tok, s, o0, o1);
-  em.cnt[oc.cls] += 1;
+  {
+    const uint64_t inc = 1ull << (21 * (oc.cls % 3u));
+    em.c0 += oc.cls < 3u ? inc : 0ull; em.c1 += (oc.cls >= 3u && oc.cls < 6u) ? inc : 0ull; em.c2 += oc.cls >= 6u ? inc : 0ull;
+  }
   if (kMode < 2) { em.ins_at += 1; return; }
 
   FfbInsRec rec;
@@ -755,7 +758,7 @@ FFB_D LineSummary walk_line(const uint8_t* s, int b, int e, bool pending_in, int
 // ---- the kernel --------------------------------------------------------------------------------
 // kRecords: also write FfbInsRec / FfbLabelRec (and the optional span / decl records)
 template <bool kRecords>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, 4)      // 4 CTAs (32 warps) per SM: cap registers at 64
 lex_corpus_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
@@ -802,8 +805,7 @@ lex_corpus_kernel(LexArgs a) {
     em.ins_limit = (kRecords && a.ins_cap) ? em.ins_at + a.ins_cap[seg] : 0x7fffffffffffffffLL;
     em.lab_limit = (kRecords && a.lab_cap) ? em.lab_at + a.lab_cap[seg] : 0x7fffffffffffffffLL;
     em.dcl_at = 0;
-#pragma unroll
-    for (int c = 0; c < FFB_N_CLASSES; ++c) em.cnt[c] = 0;
+    em.c0 = em.c1 = em.c2 = 0;
     em.shared_bytes = 0; em.regs = 0;
 
     while (phase != PH_DONE && status == FFB_OK && cur < seg_end) {
@@ -1113,7 +1115,10 @@ lex_corpus_kernel(LexArgs a) {
       status = FFB_E_CAPACITY;            // single-pass mode: the segment outgrew its record slots
     uint32_t tot[FFB_N_CLASSES];
 #pragma unroll
-    for (int c = 0; c < FFB_N_CLASSES; ++c) tot[c] = (uint32_t)warp_sum_u64(em.cnt[c]);
+    for (int c = 0; c < FFB_N_CLASSES; ++c) {
+      const uint64_t word = c < 3 ? em.c0 : (c < 6 ? em.c1 : em.c2);
+      tot[c] = (uint32_t)warp_sum_u64((word >> (21 * (c % 3))) & 0x1fffffull);
+    }
     const unsigned long long sh = warp_sum_u64(em.shared_bytes), rg = warp_sum_u64(em.regs);
     if (lane == 0) {
 #pragma unroll

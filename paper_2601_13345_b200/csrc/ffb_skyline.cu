@@ -121,8 +121,11 @@ FFB_D double block_reduce_min(double v, double* part) {
 }
 FFB_D double block_reduce_max(double v, double* part) { return -block_reduce_min(-v, part); }
 
+// IT: storage type of in-group indices (uint16_t when the group has at most 65535 points)
+template <typename IT>
 __global__ void __launch_bounds__(kThreads)
 skyline_group_kernel(SkyArgs a) {
+  constexpr uint32_t kPadI = (uint32_t)(IT)~(IT)0;
   FFB_DYN_SMEM(smem_raw);
   __shared__ double s_part[kThreads / 32 + 1];
   __shared__ unsigned long long s_bmin[kBuckets];
@@ -140,9 +143,9 @@ skyline_group_kernel(SkyArgs a) {
   double* s_e = reinterpret_cast<double*>(smem_raw);
   double* s_t = s_e + (a.resident ? a.group_size : 0);
   double* s_pm = s_t + (a.resident ? a.group_size : 0);
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_pm + MC);
-  uint32_t* s_gs = s_idx + a.sort_cap;
-  uint16_t* s_tie = reinterpret_cast<uint16_t*>(s_gs + MC);
+  uint32_t* s_gs = reinterpret_cast<uint32_t*>(s_pm + MC);
+  IT* s_idx = reinterpret_cast<IT*>(s_gs + MC);
+  uint16_t* s_tie = reinterpret_cast<uint16_t*>(s_idx + a.sort_cap + (a.sort_cap & 1));
 
   const double* ge = a.e + p0;
   const double* gt = a.t + p0;
@@ -227,7 +230,7 @@ skyline_group_kernel(SkyArgs a) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (keep) {
       const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
-      if (pos < (unsigned)MC) s_idx[pos] = (uint32_t)i;
+      if (pos < (unsigned)MC) s_idx[pos] = (IT)i;
     }
   }
   __syncthreads();
@@ -241,7 +244,7 @@ skyline_group_kernel(SkyArgs a) {
   }
   int m2 = 1;
   while (m2 < (int)m_surv) m2 <<= 1;
-  for (int i = m_surv + tid; i < m2; i += kThreads) s_idx[i] = kPad;
+  for (int i = m_surv + tid; i < m2; i += kThreads) s_idx[i] = (IT)kPadI;
   __syncthreads();
 
   // ---- 5. bitonic sort of survivors by (e, t, tie) ----
@@ -252,22 +255,41 @@ skyline_group_kernel(SkyArgs a) {
     return (uint64_t)i;
   };
   auto less = [&](uint32_t x, uint32_t y) -> bool {
-    if (x == kPad) return false;
-    if (y == kPad) return true;
+    if (x == kPadI) return false;
+    if (y == kPadI) return true;
     const double ex = pe[x], ey = pe[y];
     if (ex != ey) return ex < ey;
     const double tx = pt[x], ty = pt[y];
     if (tx != ty) return tx < ty;
     return tie_of(x) < tie_of(y);
   };
-  for (int k = 2; k <= m2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int p = tid; p < (m2 >> 1); p += kThreads) {      // one compare-exchange per pair
-        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
-        const int ixj = i | j;
-        const uint32_t x = s_idx[i], y = s_idx[ixj];
-        const bool asc = (i & k) == 0;
-        if (less(y, x) == asc) { s_idx[i] = y; s_idx[ixj] = x; }
+  // Stages with partner distance >= 64 synchronise the CTA; the remaining ones (32..1) of a
+  // level stay inside 64-element chunks, one warp per chunk, with warp-level barriers only.
+  {
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int k = 2; k <= m2; k <<= 1) {
+      int j = k >> 1;
+      for (; j >= 64; j >>= 1) {
+        for (int p = tid; p < (m2 >> 1); p += kThreads) {      // one compare-exchange per pair
+          const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+          const int ixj = i | j;
+          const uint32_t x = s_idx[i], y = s_idx[ixj];
+          const bool asc = (i & k) == 0;
+          if (less(y, x) == asc) { s_idx[i] = (IT)y; s_idx[ixj] = (IT)x; }
+        }
+        __syncthreads();
+      }
+      for (int c0 = wid * 64; c0 < m2; c0 += (kThreads / 32) * 64) {
+        for (int j2 = j; j2 > 0; j2 >>= 1) {
+          const int i = c0 + (((lane & ~(j2 - 1)) << 1) | (lane & (j2 - 1)));
+          const int ixj = i | j2;
+          if (ixj < m2) {
+            const uint32_t x = s_idx[i], y = s_idx[ixj];
+            const bool asc = (i & k) == 0;
+            if (less(y, x) == asc) { s_idx[i] = (IT)y; s_idx[ixj] = (IT)x; }
+          }
+          __syncwarp();
+        }
       }
       __syncthreads();
     }
@@ -337,14 +359,15 @@ struct Plan { int resident; int surv_cap; int sort_cap; int tie_smem; size_t sme
 Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie) {
   Plan p;
   const size_t limit = ctx->smem_optin ? ctx->smem_optin - 4096 : 96 * 1024;
-  auto need = [](int64_t mc, bool resident, int64_t g) {
-    int64_t sc = 32; while (sc < mc) sc <<= 1;
-    return (size_t)(mc * 12 + sc * 4 + (resident ? g * 16 : 0) + 64);
+  const int64_t idx_bytes = group_size <= 65535 ? 2 : 4;
+  auto need = [idx_bytes](int64_t mc, bool resident, int64_t g) {
+    int64_t sc = 64; while (sc < mc) sc <<= 1;
+    return (size_t)(mc * 12 + sc * idx_bytes + (resident ? g * 16 : 0) + 64);
   };
   int64_t mc = group_size < 32 ? 32 : group_size;
   p.resident = need(mc, true, group_size) <= limit ? 1 : 0;
   if (!p.resident) { while (mc > 1024 && need(mc, false, group_size) > limit) mc = mc / 2; }
-  int64_t sc = 32; while (sc < mc) sc <<= 1;
+  int64_t sc = 64; while (sc < mc) sc <<= 1;
   p.surv_cap = (int)mc; p.sort_cap = (int)sc;
   p.smem = need(mc, p.resident != 0, group_size);
   p.tie_smem = 0;
@@ -362,8 +385,13 @@ int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t
   a.sort_cap = p.sort_cap;
   a.tie_smem = p.tie_smem;
   if (n_groups > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "skyline: too many groups for one launch");
-  FFB_CUDA(ctx, cudaFuncSetAttribute(skyline_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-  FFB_LAUNCH(skyline_group_kernel, (unsigned)n_groups, kThreads, p.smem, stream, a);
+  if (a.group_size <= 65535) {
+    FFB_CUDA(ctx, cudaFuncSetAttribute(skyline_group_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    FFB_LAUNCH(skyline_group_kernel<uint16_t>, (unsigned)n_groups, kThreads, p.smem, stream, a);
+  } else {
+    FFB_CUDA(ctx, cudaFuncSetAttribute(skyline_group_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    FFB_LAUNCH(skyline_group_kernel<uint32_t>, (unsigned)n_groups, kThreads, p.smem, stream, a);
+  }
   return ffb_check_launch(ctx, "skyline_group_kernel");
 }
 

@@ -219,6 +219,26 @@ def main():
                        "cfg": [[p.config.block_x, p.config.block_y, p.config.p_cap] for p in preds],
                        "front": [idx[id(p)] for p in front], "t_peak": hx(brute.t_peak)})
     (HERE / "ref_pareto.json").write_text(json.dumps(clouds, indent=0))
+    # CLI reports of the reference (pkg/src/ptxwatt/cli.py) for byte-identity checks
+    from ptxwatt import cli as rcli
+    import contextlib, io
+    cli_cases = []
+    with tempfile.TemporaryDirectory() as td:
+        for fx in ("vecadd", "mha_like"):
+            ptx = Path(td) / f"{fx}.ptx"
+            ptx.write_text(fixtures[fx])
+            for argv in (["analyze", str(ptx), "--block-x", "64", "--block-y", "2", "--shared-mem-bytes", "1024"],
+                         ["predict", str(ptx), "--block-x", "32", "--block-y", "4", "--p-cap", "180", "--seq-len", "256"],
+                         ["explore", str(ptx), "--caps", "100,150,200,250", "--rho", "0.9"],
+                         ["explore", str(ptx), "--dims", "1,2,4,8,16,32,64,128", "--format", "json", "--resource-rule", "generic"],
+                         ["predict", str(ptx), "--block-x", "5", "--block-y", "5"],
+                         ["explore", str(ptx), "--seq-len", "100000"]):
+                out, err = io.StringIO(), io.StringIO()
+                with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+                    rc = rcli.main(list(argv))
+                cli_cases.append({"fixture": fx, "argv": argv[:1] + ["@PTX@"] + argv[2:], "rc": rc,
+                                  "stdout": out.getvalue(), "stderr": err.getvalue().replace(str(ptx), "@PTX@")})
+    (HERE / "ref_cli.json").write_text(json.dumps(cli_cases, indent=0))
     print("golden vectors written:", sorted(p.name for p in HERE.glob("*.json")))
 
 
