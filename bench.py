@@ -201,10 +201,10 @@ def main():
     h_front_off = torch.empty((K,), dtype=torch.int64).pin_memory()
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    phase_ms = {"lex": 0.0, "score": 0.0, "front": 0.0}
+    phase_ms = {"lex": 0.0, "flow": 0.0, "score": 0.0, "front": 0.0}
 
     def step(resident: bool, timed: bool):
-        marks = [ev() for _ in range(4)] if timed else None
+        marks = [ev() for _ in range(5)] if timed else None
         feat, res = d_feat, d_res
         if not resident:
             feat = h_feat.to(dev, non_blocking=True)
@@ -212,7 +212,9 @@ def main():
         if timed:
             marks[0].record()
         if corpus is not None:
-            feat = lex_state.run(resident=resident)          # corpus -> feature rows (device)
+            feat = lex_state.run(resident=resident, mark=marks[4] if timed else None)   # corpus -> feature rows
+        elif timed:
+            marks[4].record()
         if timed:
             marks[1].record()
         r = engine.score_grid(feat, res, sp, shp, CAPS, want=("t", "e"), out=bufs, check=False, rt=rt)
@@ -251,9 +253,10 @@ def main():
             tms = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(tms, op=dist.ReduceOp.MAX)
             ms = float(tms.item())
-        per = {"lex": 0.0, "score": 0.0, "front": 0.0}
+        per = {"lex": 0.0, "flow": 0.0, "score": 0.0, "front": 0.0}
         for m in all_marks:
-            per["lex"] += m[0].elapsed_time(m[1])
+            per["lex"] += m[0].elapsed_time(m[4])
+            per["flow"] += m[4].elapsed_time(m[1])
             per["score"] += m[1].elapsed_time(m[2])
             per["front"] += m[2].elapsed_time(m[3])
         return ms, {k: v / steps for k, v in per.items()}, rt.launches() - launches0
@@ -296,15 +299,18 @@ def main():
                   "bytes_per_unit": "16 B read per candidate (e, t f64)"},
     }
     if corpus is not None:
-        kernels["lex"] = {"kernel": "lex_corpus_kernel (+ flow)", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
+        kernels["lex"] = {"kernel": "lex_corpus_kernel", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
                           "bytes_per_unit": "1 B read per PTX byte"}
+        n_ins = int(lex_state.lex.info_i32()[:, 1].sum().item())
+        kernels["flow"] = {"kernel": "flow_kernel", "bytes": 64.0 * n_ins, "ms": phase_ms["flow"],
+                           "bytes_per_unit": "64 B read per instruction record"}
     for v in kernels.values():
         v["achieved_gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
         v["frac"] = v["achieved_gbs"] / peak if v["achieved_gbs"] else None
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     traffic = None
     try:
-        traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(kernels[dom]["kernel"])
+        traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(kernels[dom]["kernel"])   # bytes per launch, ncu
     except (OSError, ValueError):
         pass
     roofline = {"bound": "hbm", "kernel": kernels[dom]["kernel"], "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
@@ -336,7 +342,8 @@ def main():
                    "ptx_bytes_per_gpu": lex_bytes_rank, "front_points_per_gpu": front_total,
                    "l2": "no flush needed: each step streams 2.0 GB of outputs + the corpus, far above the 126 MB L2"},
         "phases_ms": phase_ms,
-        "ptx_gb_per_s": (lex_bytes_rank * world / (phase_ms["lex"] / 1e3) / 1e9) if corpus is not None and phase_ms["lex"] > 0 else None,
+        "ptx_gb_per_s": (lex_bytes_rank * world / ((phase_ms["lex"] + phase_ms["flow"]) / 1e3) / 1e9) if corpus is not None and phase_ms["lex"] > 0 else None,
+        "ptx_gb_per_s_lexer_only": (lex_bytes_rank * world / (phase_ms["lex"] / 1e3) / 1e9) if corpus is not None and phase_ms["lex"] > 0 else None,
         "clocks": clocks, "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": "configs/s",
                 "h2d_bytes_per_step": int(h_feat.numel() * 8 + h_res.numel() * 8 + lex_bytes_rank) * world,

@@ -312,11 +312,13 @@ class BenchLexState:
             self.host_text.copy_(self.corp.text)
         return self.host_text
 
-    def run(self, resident: bool = True) -> torch.Tensor:
+    def run(self, resident: bool = True, mark=None) -> torch.Tensor:
         rt, corp = self.rt, self.corp
         if not resident:
             corp.text.copy_(self.pin_host(), non_blocking=True)           # H2D inside the timed region
         lex_records_single_pass(corp, out=self.lex, rt=rt)                # K1: histogram + records
+        if mark is not None:
+            mark.record()
         kernel_features(corp, self.lex, out_feat=self.feat, rt=rt)        # K1b
         return self.feat
 

@@ -758,7 +758,7 @@ FFB_D LineSummary walk_line(const uint8_t* s, int b, int e, bool pending_in, int
 // ---- the kernel --------------------------------------------------------------------------------
 // kRecords: also write FfbInsRec / FfbLabelRec (and the optional span / decl records)
 template <bool kRecords>
-__global__ void __launch_bounds__(kWarps * 32, 4)      // 4 CTAs (32 warps) per SM: cap registers at 64
+__global__ void __launch_bounds__(kWarps * 32, kRecords ? 2 : 4)   // record mode needs ~128 registers (measured: capping at 64 spills and is 1.5x slower)
 lex_corpus_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
