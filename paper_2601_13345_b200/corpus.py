@@ -50,6 +50,7 @@ class Corpus:
     order: torch.Tensor | None = None   # int32 [K] longest-first processing order
     host_text: bytes | None = None
     host_off: np.ndarray | None = None
+    kernel_mask: np.ndarray | None = None   # split_modules: False for gap segments that hold no kernel
 
     @property
     def padded_bytes(self) -> int:
@@ -337,3 +338,64 @@ def smoke_check(rt: native.Runtime) -> None:
         assert status[k] == 0 and hist[k].tolist() == orc.class_histogram(kern), f"histogram differs (kernel {k})"
         want = np.asarray(orc.kernel_feature_row(src), dtype=np.float64)
         assert feat[k, :11].tobytes() == want.tobytes(), f"feature row differs (kernel {k})"
+
+
+# ------------------------------------------------------------------------------ multi-kernel modules
+def split_modules(text: bytes, module_off: np.ndarray | None = None, *, max_kernels_per_module: int = 1 << 16,
+                  rt: native.Runtime | None = None) -> Corpus:
+    """One corpus segment per ``.entry`` kernel of every module.
+
+    The reference parses ONE kernel per ``parse_ptx`` call (first or named, ptx.py:168-184); here
+    round i lexes the i-th kernel of every module at once (histogram mode stops at the closing
+    brace of the kernel body) and the next round resumes right behind it, so the whole corpus is
+    read once.  Segment k then behaves like ``parse_ptx(module, kernel_name=<k-th name>)`` — same
+    instructions, labels and features; only ``source_line`` is relative to the segment.
+    """
+    rt = rt or native.get_runtime()
+    n = len(text)
+    module_off = np.asarray([0, n] if module_off is None else module_off, dtype=np.int64)
+    whole = upload_corpus(text, module_off, balance=False, rt=rt)
+    starts, ends = module_off[:-1].copy(), module_off[1:].copy()
+    alive = np.arange(len(starts))
+    pieces: list[tuple[int, int, int]] = []          # (module, start, stop)
+    for _ in range(max_kernels_per_module):
+        if alive.size == 0:
+            break
+        seg = np.empty(2 * alive.size, dtype=np.int64)
+        seg[0::2], seg[1::2] = starts[alive], ends[alive]
+        # alternate "kernel remainder" / "gap" segments keep the table ascending; gaps are empty or ignored
+        table = np.concatenate([seg, [ends[alive[-1]]]])
+        round_corp = Corpus(text=whole.text, n_bytes=whole.n_bytes, seg_off=rt.to_device(torch.from_numpy(table)),
+                            n_segs=len(table) - 1, order=None)
+        info = lex_histogram(round_corp, rt=rt).info_np()[0::2]
+        nxt = []
+        for m, inf in zip(alive, info):
+            if int(inf["status"]) == 2:              # NoKernelFound: module exhausted
+                continue
+            if int(inf["status"]) != 0 or int(inf["body_end"]) == 0:
+                # malformed kernel: keep the remainder as one segment so the error is reported, stop this module
+                pieces.append((int(m), int(starts[m]), int(ends[m])))
+                continue
+            stop = int(starts[m]) + int(inf["body_end"]) + 1
+            pieces.append((int(m), int(starts[m]), stop))
+            starts[m] = stop
+            nxt.append(m)
+        alive = np.asarray(nxt, dtype=np.int64)
+    pieces.sort(key=lambda p: p[1])
+    if not pieces:
+        return Corpus(text=whole.text, n_bytes=n, seg_off=rt.to_device(torch.zeros(1, dtype=torch.int64)), n_segs=0)
+    # consecutive pieces of one module are contiguous; pieces of different modules may leave gaps,
+    # which become (kernel-less) segments of their own so that the table stays a partition
+    bounds = [pieces[0][1]]
+    keep = []
+    for _, a, b in pieces:
+        if a != bounds[-1]:
+            bounds.append(a)
+            keep.append(False)
+        bounds.append(b)
+        keep.append(True)
+    seg_off = np.asarray(bounds, dtype=np.int64)
+    corp = Corpus(text=whole.text, n_bytes=n, seg_off=rt.to_device(torch.from_numpy(seg_off)), n_segs=len(seg_off) - 1,
+                  host_text=text, host_off=seg_off)
+    corp.kernel_mask = np.asarray(keep, dtype=bool)      # False for gap segments
+    return corp

@@ -97,8 +97,10 @@ FFB_D unsigned long long warp_sum_u64(unsigned long long v) {
 FFB_D int next_bit(const uint32_t m[4], int from);
 
 // ---- T1: comment automaton ------------------------------------------------------------------
-FFB_D int cm_step(int st, unsigned c) {
-  const bool sl = c == '/', star = c == '*', nl = c == '\n';
+// allow_block = false: "/*" no longer opens a comment (the reference's regex only matches a
+// "/*" that has a closing "*/" somewhere behind it, ptx.py:140)
+FFB_D int cm_step(int st, unsigned c, bool allow_block) {
+  const bool sl = c == '/', star = c == '*' && allow_block, nl = c == '\n';
   switch (st) {
     case S_CODE: return sl ? S_SLASH : S_CODE;
     case S_SLASH: return star ? S_BLK : (sl ? S_SLASH2 : S_CODE);
@@ -114,14 +116,18 @@ FFB_D int cm_step(int st, unsigned c) {
 
 // Runs the automaton over s[c0,c1) from state `st`; when `blank` is set rewrites comment
 // bytes to ' ' (newlines inside block comments become kNlInBlock).  Returns the exit state.
-FFB_D int cm_run(uint8_t* s, int c0, int c1, int st, bool blank, const uint32_t slash[4], int chunk_base) {
+// noblk_from: first position whose "/*" must NOT open a comment; last_open: position of the
+// last "/*" that did open one (for the unterminated-comment fix-up).
+FFB_D int cm_run(uint8_t* s, int c0, int c1, int st, bool blank, const uint32_t slash[4], int chunk_base,
+                 int noblk_from, int* last_open) {
   for (int i = c0; i < c1; ++i) {
     if (st == S_CODE) {                       // nothing happens in code until the next '/'
       i = chunk_base + next_bit(slash, i - chunk_base);
       if (i >= c1) break;
     }
     const unsigned c = s[i];
-    const int nx = cm_step(st, c);
+    const int nx = cm_step(st, c, i - 1 < noblk_from);
+    if (nx >= S_BLK && st < S_BLK) *last_open = i - 1;
     if (blank) {
       const bool in_blk = st >= S_BLK;
       if (in_blk) {
@@ -787,6 +793,8 @@ lex_corpus_kernel(LexArgs a) {
     // ---- warp-uniform segment state ----
     int phase = PH_SEARCH;
     int cm_state = S_CODE;            // comment automaton state at `cur`
+    int64_t noblk_from_g = 0x7fffffffffffffffLL;   // from here on "/*" is plain text (unterminated comment)
+    int64_t blk_close_g = -1;         // a "*/" is known to exist up to here
     int depth = 0;
     bool pending = false;             // ptx.py's `pending` string is non-empty
     uint32_t line_no = 1;             // source line of the byte at `cur`
@@ -833,14 +841,17 @@ lex_corpus_kernel(LexArgs a) {
       uint32_t slash[4], unused4[4];
       chunk_masks(s + chunk_base, 0x2f2f2f2fu, 0x2f2f2f2fu, c0 - chunk_base, c1 - chunk_base, slash, unused4);
       const bool has_slash = (slash[0] | slash[1] | slash[2] | slash[3]) != 0;
-      int st_in = S_CODE, st_out = S_CODE;
-      {
+      int st_in = S_CODE, st_out = S_CODE, last_open = -1;
+      int noblk_from = noblk_from_g >= abase + kTile ? 0x7fffffff : (noblk_from_g <= abase ? 0 : (int)(noblk_from_g - abase));
+      for (int attempt = 0; attempt < 2; ++attempt) {
         bool need = true;
+        st_in = S_CODE;
         for (int guard = 0; guard < 40; ++guard) {
           if (need) {
+            last_open = -1;
             if (c0 >= c1) st_out = st_in;
             else if (!has_slash && st_in == S_CODE) st_out = S_CODE;
-            else st_out = cm_run(s, c0, c1, st_in, false, slash, chunk_base);
+            else st_out = cm_run(s, c0, c1, st_in, false, slash, chunk_base, noblk_from, &last_open);
             need = false;
           }
           int left = __shfl_up_sync(kFull, st_out, 1);
@@ -849,10 +860,30 @@ lex_corpus_kernel(LexArgs a) {
           if (!__any_sync(kFull, changed)) break;
           if (changed) { st_in = left; need = true; }
         }
+        // a block comment still open at the tile end must have its "*/" somewhere behind
+        const int end_state = __shfl_sync(kFull, st_out, 31);
+        if (end_state < S_BLK || attempt == 1 || blk_close_g >= abase + hi) break;
+        int64_t found = -1;
+        const int64_t from = abase + hi - ((end_state == S_BLK_STAR || end_state == S_LBLK_STAR) ? 1 : 0);
+        for (int64_t g0 = from; g0 < seg_end - 1 && found < 0; g0 += 32) {
+          const int64_t g = g0 + lane;
+          const bool hit = g + 1 < seg_end && a.text[g] == '*' && a.text[g + 1] == '/';
+          const unsigned mask = __ballot_sync(kFull, hit);
+          if (mask) found = g0 + __ffs((int)mask) - 1;
+        }
+        if (found >= 0) { blk_close_g = found + 2; break; }
+        // unterminated: the last "/*" of this tile and everything behind it is ordinary text
+        int lo_open = last_open;
+#pragma unroll
+        for (int dd = 16; dd > 0; dd >>= 1) { const int o = __shfl_xor_sync(kFull, lo_open, dd); lo_open = o > lo_open ? o : lo_open; }
+        if (lo_open < 0) break;                       // opened in an earlier tile: cannot happen, keep going
+        noblk_from_g = abase + lo_open;
+        noblk_from = lo_open;
       }
       const bool dirty = (has_slash || st_in != S_CODE) && c0 < c1;
       if (__any_sync(kFull, dirty)) {
-        if (dirty) cm_run(s, c0, c1, st_in, true, slash, chunk_base);
+        int dummy = -1;
+        if (dirty) cm_run(s, c0, c1, st_in, true, slash, chunk_base, noblk_from, &dummy);
         __syncwarp();
       }
 

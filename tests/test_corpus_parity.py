@@ -96,3 +96,33 @@ def test_single_pass_records_equal_two_pass(backend):
     assert (st2 == 0).all() and (st1[:-1] == 0).all() and st1[-1] == 11
     assert np.array_equal(lex1.hist.cpu().numpy(), lex2.hist.cpu().numpy())
     assert fl1.feat.cpu().numpy()[:-1, :11].tobytes() == fl2.feat.cpu().numpy()[:-1, :11].tobytes()
+
+
+def test_multi_kernel_module_ingestion(backend):
+    """split_modules: every .entry of every module becomes a segment whose feature row equals the
+    oracle's parse of the whole module with that kernel named (reference: ptx.py:168-184)."""
+    text, offs = synth.ptx_corpus(seed=17, n_kernels=7, lo=20, hi=120, comments=True)
+    segs = [text[offs[i]:offs[i + 1]].decode() for i in range(7)]
+    mod_a = ".version 8.0\n.func helper()\n{\n ret;\n}\n" + "".join(segs[:3]) + "// trailing\n"
+    mod_b = "".join(segs[3:]) + ".global .u32 tail;\n"
+    mod_c = "// a module without kernels\n.func f() { ret; }\n"
+    blob = (mod_a + mod_b + mod_c).encode()
+    module_off = np.cumsum([0, len(mod_a), len(mod_b), len(mod_c)])
+    corp = corpus.split_modules(blob, module_off)
+    mask = corp.kernel_mask
+    assert int(mask.sum()) == 7
+    lex, fl = corpus.analyze_corpus(corp)
+    info, feat, status = lex.info_np(), fl.feat.cpu().numpy(), fl.status.cpu().numpy()
+    names, k = [], 0
+    seg_off = corp.host_off
+    for s_i in range(corp.n_segs):
+        if not mask[s_i]:
+            continue
+        module_src = mod_a if k < 3 else mod_b
+        piece = blob[seg_off[s_i]:seg_off[s_i + 1]]
+        name = piece[int(info[s_i]["name_off"]): int(info[s_i]["name_off"]) + int(info[s_i]["name_len"])].decode()
+        want = np.asarray(orc.kernel_feature_row(module_src, wanted=name), dtype=np.float64)
+        assert status[s_i] == 0 and feat[s_i, :11].tobytes() == want.tobytes(), name
+        names.append(name)
+        k += 1
+    assert len(set(names)) == 7
