@@ -22,6 +22,10 @@
 // instruction for the dataflow kernel (K1b).
 #include "ffb_records.cuh"
 
+// rarely taken, register-hungry paths are kept out of line so that the hot loop of the lexer
+// is allocated for the common case only
+#define FFB_COLD __device__ __forceinline__
+
 namespace {
 
 constexpr int kWarps = 8;
@@ -36,10 +40,11 @@ constexpr uint8_t kNlInBlock = 0x8A;        // newline that sits inside a /* */ 
 enum Phase { PH_SEARCH = 0, PH_HEADER, PH_BODY, PH_DONE };
 
 // byte classes of the per-line feature scan
-enum { CC_WS = 1, CC_SEMI = 2, CC_LBRACE = 4, CC_RBRACE = 8, CC_COLON = 16, CC_LABEL = 32 };
+enum { CC_WS = 1, CC_SEMI = 2, CC_LBRACE = 4, CC_RBRACE = 8, CC_COLON = 16, CC_LABEL = 32, CC_OPEN = 64, CC_CLOSE = 128 };
 FFB_HD uint8_t char_class(unsigned c) {
   return (uint8_t)((ffb_is_ws(c) ? CC_WS : 0) | (c == ';' ? CC_SEMI : 0) | (c == '{' ? CC_LBRACE : 0) |
-                   (c == '}' ? CC_RBRACE : 0) | (c == ':' ? CC_COLON : 0) | (ffb_is_label_char(c) ? CC_LABEL : 0));
+                   (c == '}' ? CC_RBRACE : 0) | (c == ':' ? CC_COLON : 0) | (ffb_is_label_char(c) ? CC_LABEL : 0) |
+                   ((c == '[' || c == '{' || c == '(') ? CC_OPEN : 0) | ((c == ']' || c == '}' || c == ')') ? CC_CLOSE : 0));
 }
 // what the feature scan makes of a line (anything it cannot prove simple is LK_COMPLEX and
 // takes the general statement walk)
@@ -341,7 +346,7 @@ FFB_D bool span_ends(const uint8_t* s, int a, int b, const char* lit, int n) {
 }
 
 // Python int(text, 0) on s[a,b) (already stripped).  0: not a literal, 1: value in *out, 2: too big.
-FFB_D int py_int_literal(const uint8_t* s, int a, int b, int64_t* out) {
+FFB_COLD int py_int_literal(const uint8_t* s, int a, int b, int64_t* out) {
   int i = a;
   bool neg = false;
   if (i < b && (s[i] == '+' || s[i] == '-')) { neg = s[i] == '-'; ++i; }
@@ -403,7 +408,7 @@ FFB_D uint64_t describe_operand(const uint8_t* s, int a, int b) {
 
 // alignment.py:21 address regex on the operand s[a,b) (starts with '[').  Returns the address
 // kind and, for registers, the descriptor of the base name.
-FFB_D uint32_t describe_address(const uint8_t* s, int a, int b, uint64_t* desc) {
+FFB_COLD uint32_t describe_address(const uint8_t* s, int a, int b, uint64_t* desc) {
   *desc = 0;
   if (b - a < 2 || s[b - 1] != ']') return FFB_ADDR_NOMATCH;
   const int i0 = a + 1, i1 = b - 1;
@@ -458,7 +463,7 @@ FFB_D uint32_t type_bytes(const uint8_t* s, int a, int b, uint32_t dflt) {
   }
 }
 // `.reg .cls %name<N>` -> count in *n, class token span in [*c0,*c1); false if not a match.
-FFB_D bool parse_reg_decl(const uint8_t* s, int a, int e, uint64_t* n, int* c0, int* c1) {
+FFB_COLD bool parse_reg_decl(const uint8_t* s, int a, int e, uint64_t* n, int* c0, int* c1) {
   if (e - a < 4 || !span_eq(s, a, a + 4, ".reg", 4)) return false;
   int i = scan_ws(s, a + 4, e);
   if (i == a + 4 || i >= e || s[i] != '.') return false;
@@ -476,7 +481,7 @@ FFB_D bool parse_reg_decl(const uint8_t* s, int a, int e, uint64_t* n, int* c0, 
   return true;
 }
 // `.shared [.align N] .type name[N]` -> bytes; false if not a match.
-FFB_D bool parse_shared_decl(const uint8_t* s, int a, int e, uint64_t* bytes) {
+FFB_COLD bool parse_shared_decl(const uint8_t* s, int a, int e, uint64_t* bytes) {
   if (e - a < 7 || !span_eq(s, a, a + 7, ".shared", 7)) return false;
   int i = scan_ws(s, a + 7, e);
   if (i == a + 7) return false;
@@ -518,6 +523,7 @@ struct Emit {
   // where this lane's results go (record mode) and its accumulators
   const LexArgs* a;
   TokTable tok;          // shared-memory token table
+  const uint8_t* cls;    // shared-memory byte-class table
   int64_t seg;            // segment index
   int64_t seg_begin;      // global offset of the segment
   int64_t abase;          // global offset of smem index 0
@@ -598,10 +604,8 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
   const bool aux_is_op4 = !is_mem && oc.cls != FFB_CLS_BRANCH;
   for (int q = o1; q <= e; ++q) {
     const unsigned c = q < e ? s[q] : 0u;
-    if (q < e) {
-      if (c == '[' || c == '{' || c == '(') ++depth;
-      else if (c == ']' || c == '}' || c == ')') --depth;
-    }
+    const unsigned kc = q < e ? em.cls[c] : 0u;
+    depth += (int)((kc >> 6) & 1u) - (int)((kc >> 7) & 1u);
     if (q == e || (c == ',' && depth == 0)) {
       if (ps >= 0) {
         if (count == 0) { s0 = ps; e0 = pe; } else if (count == 1) { s1 = ps; e1 = pe; }
@@ -617,7 +621,7 @@ FFB_D void do_statement(const uint8_t* s, int b, int e, Emit& em) {
         ++count;
       }
       ps = -1;
-    } else if (!ffb_is_ws(c)) {
+    } else if (!(kc & CC_WS)) {
       if (ps < 0) ps = q;
       pe = q + 1;
     }
@@ -673,7 +677,7 @@ FFB_D void do_directive(const uint8_t* s, int b, int e, Emit& em, int* n_decl) {
 // end).  pending_in: the line starts inside an unfinished statement.  hi/depth_in serve the
 // look-ahead of a statement this line opens.  kMode 0 only fills the summary.
 template <int kMode>
-FFB_D LineSummary walk_line(const uint8_t* s, int b, int e, bool pending_in, int hi, int depth_in,
+FFB_COLD LineSummary walk_line(const uint8_t* s, int b, int e, bool pending_in, int hi, int depth_in,
                             bool at_seg_end, Emit& em) {
   LineSummary r;
   r.nonblank = r.has_semi = r.pend_out0 = r.defer = r.unterminated = false;
@@ -807,7 +811,7 @@ lex_corpus_kernel(LexArgs a) {
 
     Emit em;
     em.a = &a; em.seg = seg; em.seg_begin = seg_begin; em.abase = 0; em.line = 0;
-    em.tok.key = s_tok_key; em.tok.val = s_tok_val;
+    em.tok.key = s_tok_key; em.tok.val = s_tok_val; em.cls = s_cls;
     em.ins_at = kRecords ? a.ins_base[seg] : 0;
     em.lab_at = kRecords ? a.lab_base[seg] : 0;
     em.ins_limit = (kRecords && a.ins_cap) ? em.ins_at + a.ins_cap[seg] : 0x7fffffffffffffffLL;
@@ -987,15 +991,24 @@ lex_corpus_kernel(LexArgs a) {
             int maxlen = len;
 #pragma unroll
             for (int dd = 16; dd > 0; dd >>= 1) { const int o = __shfl_xor_sync(kFull, maxlen, dd); maxlen = o > maxlen ? o : maxlen; }
-            int fb = -1, lb = -1, n_semi = 0, n_colon = 0, n_labch = 0, n_nonws = 0;
-            int run = 0, min_run = 0x7fffffff;
+            int fb = 0x7fffffff, lb = -1, n_semi = 0, n_colon = 0, n_nonws = 0;
+            unsigned seen = 0;
             for (int i = 0; i < maxlen; ++i) {
               if (i < len) {
                 const unsigned k = s_cls[s[b + i]];
-                if (!(k & CC_WS)) { if (fb < 0) fb = b + i; lb = b + i; ++n_nonws; }
-                n_semi += (k >> 1) & 1; n_colon += (k >> 4) & 1; n_labch += (k >> 5) & 1;
-                if (k & CC_LBRACE) ++run;
-                else if (k & CC_RBRACE) { --run; if (run < min_run) min_run = run; }
+                seen |= k;
+                n_semi += (k >> 1) & 1; n_colon += (k >> 4) & 1;
+                if (!(k & CC_WS)) { fb = min(fb, b + i); lb = b + i; ++n_nonws; }
+              }
+            }
+            if (lb < 0) fb = -1;
+            // braces are rare (vector operands, nested scopes): walk them only where they occur
+            int run = 0, min_run = 0x7fffffff;
+            if (seen & (CC_LBRACE | CC_RBRACE)) {
+              for (int i = b; i < e; ++i) {
+                const unsigned c = s[i];
+                if (c == '{') ++run;
+                else if (c == '}') { --run; if (run < min_run) min_run = run; }
               }
             }
             int tot_delta = 0;
@@ -1025,8 +1038,10 @@ lex_corpus_kernel(LexArgs a) {
                 if (n_semi == 0 && n_colon == 0 && !decl) kind = LK_SKIP;         // ptx.py:255-256
               } else if (c_last == ';' && n_semi == 1 && n_colon == 0 && lb > fb) {
                 kind = LK_STMT;       // one statement, ';' last (braces inside operands are balanced)
-              } else if (c_last == ':' && n_semi == 0 && n_colon == 1 && n_labch == n_nonws - 1 && lb - fb + 1 == n_nonws && lb > fb) {
-                kind = LK_LABEL;                                                  // ptx.py:232-236
+              } else if (c_last == ':' && n_semi == 0 && n_colon == 1 && lb - fb + 1 == n_nonws && lb > fb) {
+                bool all_label = true;                                            // ptx.py:232-236
+                for (int i = fb; i < lb && all_label; ++i) all_label = (s_cls[s[i]] & CC_LABEL) != 0;
+                if (all_label) kind = LK_LABEL;
               }
             }
             if (lane == end_lane) kind = LK_COMPLEX;
