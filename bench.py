@@ -269,6 +269,27 @@ def main():
     ms_e2e, _, _ = run(False, max(3, args.steps // 2), 2)
     e2e_steps = max(3, args.steps // 2)
 
+    # ---- K1 alone, histogram mode (north_star leg 1: text -> per-kernel class histograms) ----
+    hist_ms, path_counts = None, None
+    if corpus is not None:
+        hres = corpus_mod.lex_histogram(corpus, rt=rt)
+        for _ in range(2):
+            corpus_mod.lex_histogram(corpus, out=hres, rt=rt)
+        torch.cuda.synchronize()
+        h0, h1 = ev(), ev()
+        n_hist = max(3, args.steps)
+        h0.record()
+        for _ in range(n_hist):
+            corpus_mod.lex_histogram(corpus, out=hres, rt=rt)
+        h1.record()
+        torch.cuda.synchronize()
+        hist_ms = h0.elapsed_time(h1) / n_hist
+        if world > 1:
+            tms = torch.tensor([hist_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+            hist_ms = float(tms.item())
+        path_counts = [int(x) for x in lex_state.lex.path_counts.cpu().tolist()]
+
     points_rank = K * G
     points_total = points_rank * world
     lex_bytes_rank = int(corpus.n_bytes) if corpus is not None else 0
@@ -299,15 +320,17 @@ def main():
                   "bytes_per_unit": "16 B read per candidate (e, t f64)"},
     }
     if corpus is not None:
-        kernels["lex"] = {"kernel": "lex_corpus_kernel", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
-                          "bytes_per_unit": "1 B read per PTX byte"}
+        kernels["lex"] = {"kernel": "lex_fast_kernel<records>", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
+                          "bytes_per_unit": "1 B read per PTX byte (+ ~2 B of records written per byte)"}
+        kernels["lex_hist"] = {"kernel": "lex_fast_kernel<histogram>", "bytes": float(lex_bytes_rank), "ms": hist_ms,
+                               "bytes_per_unit": "1 B read per PTX byte", "in_step": False}
         n_ins = int(lex_state.lex.info_i32()[:, 1].sum().item())
         kernels["flow"] = {"kernel": "flow_kernel", "bytes": 64.0 * n_ins, "ms": phase_ms["flow"],
                            "bytes_per_unit": "64 B read per instruction record"}
     for v in kernels.values():
         v["achieved_gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
         v["frac"] = v["achieved_gbs"] / peak if v["achieved_gbs"] else None
-    dom = max(kernels, key=lambda k: kernels[k]["ms"])
+    dom = max((k for k in kernels if kernels[k].get("in_step", True)), key=lambda k: kernels[k]["ms"])
     traffic = None
     try:
         traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(kernels[dom]["kernel"])   # bytes per launch, ncu
@@ -344,6 +367,8 @@ def main():
         "phases_ms": phase_ms,
         "ptx_gb_per_s": (lex_bytes_rank * world / ((phase_ms["lex"] + phase_ms["flow"]) / 1e3) / 1e9) if corpus is not None and phase_ms["lex"] > 0 else None,
         "ptx_gb_per_s_lexer_only": (lex_bytes_rank * world / (phase_ms["lex"] / 1e3) / 1e9) if corpus is not None and phase_ms["lex"] > 0 else None,
+        "ptx_gb_per_s_histogram_mode": (lex_bytes_rank * world / (hist_ms / 1e3) / 1e9) if hist_ms else None,
+        "lexer_segments_fast_exact_slowstmts": path_counts,
         "clocks": clocks, "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": "configs/s",
                 "h2d_bytes_per_step": int(h_feat.numel() * 8 + h_res.numel() * 8 + lex_bytes_rank) * world,

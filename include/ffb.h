@@ -228,7 +228,15 @@ typedef struct {
                                  (the structural passes of K1b stream this instead of the records) */
   FfbSpanRec* d_spans;        /* optional, parallel to d_ins                                    */
   FfbDeclRec* d_decls;        /* optional, [K, FFB_MAX_DECLS]                                   */
+  uint32_t flags;             /* FFB_LEX_* bits                                                 */
+  uint32_t* d_path_counts;    /* optional [4]: segments finished by the fast path / by the exact walk,
+                                 statements the fast path parsed byte-serially, reserved           */
 } FfbLexDesc;
+/* Two device kernels implement K1 with identical results: a byte-parallel fast path for regular
+ * text (what compilers emit) and the exact statement walk for everything else; segments the fast
+ * path declines are handed over on the device, in the same stream.  FFB_LEX_EXACT_ONLY skips the
+ * fast path (it is also skipped for kernel-name filters and span / declaration records). */
+#define FFB_LEX_EXACT_ONLY 1u
 int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream);
 /* classify_opcode (ptx.py:99) and Instruction.access_bytes (ptx.py:64) for n opcode strings:
  * string i is d_text[d_off[i] : d_off[i+1]); d_out[n,3] = {class, state space, access bytes}. */

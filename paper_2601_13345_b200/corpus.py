@@ -36,7 +36,7 @@ class LexDesc(C.Structure):
         ("d_order", C.c_void_p), ("h_kernel_name", C.c_char_p), ("kernel_name_len", C.c_int32),
         ("d_hist", C.c_void_p), ("d_info", C.c_void_p), ("d_ins_base", C.c_void_p), ("d_lab_base", C.c_void_p),
         ("d_ins_cap", C.c_void_p), ("d_lab_cap", C.c_void_p), ("d_ins", C.c_void_p), ("d_labels", C.c_void_p), ("d_meta", C.c_void_p), ("d_spans", C.c_void_p),
-        ("d_decls", C.c_void_p),
+        ("d_decls", C.c_void_p), ("flags", C.c_uint32), ("d_path_counts", C.c_void_p),
     ]
 
 
@@ -93,6 +93,7 @@ class LexResult:
     decls: torch.Tensor | None = None    # uint8 [K, 32, 16]
     n_ins: int = 0
     n_lab: int = 0
+    path_counts: torch.Tensor | None = None   # int32 [4]: segments fast / exact, byte-serial statements, -
 
     def info_np(self) -> np.ndarray:
         return self.info.cpu().numpy().view(SEG_DTYPE).reshape(-1)
@@ -101,15 +102,21 @@ class LexResult:
         return self.info.view(torch.int32).view(-1, 12)
 
 
+LEX_EXACT_ONLY = 1
+EXACT_ONLY_DEFAULT = False      # tests flip this to run the exact statement walk alone
+
+
 def _call_lex(rt, corp: Corpus, hist, info, *, kernel_name: bytes | None = None, ins_base=None, lab_base=None,
-              ins_cap=None, lab_cap=None, ins=None, labels=None, meta=None, spans=None, decls=None):
+              ins_cap=None, lab_cap=None, ins=None, labels=None, meta=None, spans=None, decls=None,
+              exact_only: bool = False, path_counts=None):
     d = LexDesc(
         d_text=native.ptr(corp.text), n_bytes=corp.padded_bytes, d_seg_off=native.ptr(corp.seg_off),
         n_segs=corp.n_segs, d_order=native.ptr(corp.order),
         h_kernel_name=kernel_name, kernel_name_len=len(kernel_name) if kernel_name else 0,
         d_hist=native.ptr(hist), d_info=native.ptr(info), d_ins_base=native.ptr(ins_base),
         d_lab_base=native.ptr(lab_base), d_ins_cap=native.ptr(ins_cap), d_lab_cap=native.ptr(lab_cap), d_ins=native.ptr(ins), d_labels=native.ptr(labels),
-        d_meta=native.ptr(meta), d_spans=native.ptr(spans), d_decls=native.ptr(decls))
+        d_meta=native.ptr(meta), d_spans=native.ptr(spans), d_decls=native.ptr(decls),
+        flags=LEX_EXACT_ONLY if (exact_only or EXACT_ONLY_DEFAULT) else 0, d_path_counts=native.ptr(path_counts))
     rc = rt.lib.ffb_lex_corpus(rt.ctx, C.byref(d), rt.stream())
     rt.check(rc, "ffb_lex_corpus")
 
@@ -120,7 +127,10 @@ def lex_histogram(corp: Corpus, *, kernel_name: str | None = None, out: LexResul
     rt = rt or native.get_runtime()
     K = corp.n_segs
     res = out or LexResult(hist=rt.empty((K, native.N_CLASSES), torch.int32), info=rt.empty((K, 48), torch.uint8))
-    _call_lex(rt, corp, res.hist, res.info, kernel_name=kernel_name.encode() if kernel_name else None)
+    if res.path_counts is None:
+        res.path_counts = rt.empty((4,), torch.int32)
+    _call_lex(rt, corp, res.hist, res.info, kernel_name=kernel_name.encode() if kernel_name else None,
+              path_counts=res.path_counts)
     return res
 
 
@@ -144,7 +154,8 @@ def lex_records(corp: Corpus, *, kernel_name: str | None = None, spans: bool = F
     res.spans = torch.zeros((max(res.n_ins, 1), 128), dtype=torch.uint8, device=rt.device) if spans else None
     res.decls = torch.zeros((K, MAX_DECLS, 16), dtype=torch.uint8, device=rt.device) if decls else None
     _call_lex(rt, corp, res.hist, res.info, kernel_name=name, ins_base=res.ins_base, lab_base=res.lab_base,
-              ins=res.ins, labels=res.labels, meta=res.meta, spans=res.spans, decls=res.decls)
+              ins=res.ins, labels=res.labels, meta=res.meta, spans=res.spans, decls=res.decls,
+              path_counts=res.path_counts)
     return res
 
 
@@ -170,8 +181,9 @@ def lex_records_single_pass(corp: Corpus, *, bytes_per_ins: int = 12, bytes_per_
         res.ins = rt.empty((max(res.n_ins, 1), 64), torch.uint8)
         res.labels = rt.empty((max(res.n_lab, 1), 16), torch.uint8)
         res.meta = rt.empty((max(res.n_ins, 1),), torch.int32)
+        res.path_counts = rt.empty((4,), torch.int32)
     _call_lex(rt, corp, res.hist, res.info, ins_base=res.ins_base, lab_base=res.lab_base, ins_cap=res.ins_cap,
-              lab_cap=res.lab_cap, ins=res.ins, labels=res.labels, meta=res.meta)
+              lab_cap=res.lab_cap, ins=res.ins, labels=res.labels, meta=res.meta, path_counts=res.path_counts)
     return res
 
 

@@ -780,7 +780,8 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
 
 // Name hash used for annotation keys (same function as the lexer's label hash).
 extern "C" uint64_t ffb_name_hash(const uint8_t* name, int64_t len) {
-  uint64_t h = kFnvBasis;
-  for (int64_t i = 0; i < len; ++i) h = ffb_hash_step(h, name[i]);
-  return ffb_hash_fold(h);
+  FfbHasher x;
+  ffb_hash_init(x);
+  for (int64_t i = 0; i < len; ++i) ffb_hash_byte(x, name[i]);
+  return ffb_hash_done(x);
 }

@@ -1,0 +1,863 @@
+// K1 fast path: byte-parallel lexer for REGULAR segments, with a device-side hand-over of
+// everything else to the exact walk in ffb_lex.cu (same results either way; a segment is
+// finished by exactly one of the two kernels).
+//
+// "Regular" is what compilers emit and what the reference's parse_ptx (ptx.py:207-293) handles
+// without its `pending` machinery: 7-bit text whose only blanks are ' ' '\t' '\n', no "/*"
+// anywhere before the end of the kernel body, and body lines that are - after cutting a
+// trailing "// ..." comment (ptx.py:141) - one of
+//     blank | `name:` | bare `{` / `}` | `.directive [;]` | `[@p] opcode operands ;`
+// with braces inside a statement balanced.  Anything else (multi-line statements, several
+// statements on a line, label + statement on one line, block comments, CR/LF, a kernel name
+// filter ...) marks the segment; marked segments are appended to a work list that the exact
+// kernel consumes in the same stream.  No host round trip, no CPU path.
+//
+// One warp per segment (dynamic queue), 4 KB tiles:
+//   M  each lane loads eight coalesced 16-byte units and, still in registers, derives 16-bit
+//      position masks by SWAR (newline, ';', "rare" = ':' '{' '}' '/', and '.' while the
+//      kernel header is still being searched) plus a reject flag for bytes outside the
+//      regular alphabet; text and masks go to shared memory (conflict-free 16 B / 2 B stores);
+//   T  lane L owns mask words 4L..4L+3: popcounts + one warp scan give the newline table and
+//      per-word prefix counts, so "how many ';' / rare bytes in [b,e)" is two rank queries;
+//   S  `.entry NAME` and the opening '{' by warp-min over mask bits (ptx.py:165-176);
+//   P1 one lane per line: rank queries split lines into plain and careful (any rare byte);
+//      plain lines are classified from first/last byte and the ';' count;
+//      careful lines are compacted and resolved 32 at a time (comment cut, label, braces),
+//      a warp scan of the brace deltas finds the line that closes the body;
+//   P2 one lane per line again: opcode classification / 64-byte records through the same
+//      do_statement the exact kernel uses; record slots come from ballots, not atomics.
+#pragma once
+#include "ffb_lex_shared.cuh"
+
+namespace {
+
+constexpr int kFWarps = 4;
+constexpr int kFTile = 4096;
+constexpr int kFPad = 64;
+constexpr int kFWords = kFTile / 32;              // 32-byte mask words per tile
+constexpr int kFMaxLines = 256;
+// per-warp shared memory (byte offsets)
+constexpr int kFOffNlm = kFTile + kFPad;                        // u32[128] newline mask; later u16[256] careful / slow lists
+constexpr int kFOffMA = kFOffNlm + kFWords * 4;                 // uint4[128 + 4] {semi, rare, blank, dot} per 32-byte word (+ zero sentinels)
+constexpr int kFOffP = kFOffMA + (kFWords + 4) * 16;            // u32[128 + 4] prefix counts (semi | rare << 16) + total
+constexpr int kFOffNl = kFOffP + (kFWords + 4) * 4;             // u16[kFMaxLines + 8] newline positions
+constexpr int kFOffInfo = kFOffNl + (kFMaxLines + 8) * 2;       // u32[kFMaxLines] line info
+constexpr int kFOffMB = kFOffInfo + kFMaxLines * 4;             // record mode: uint4[128 + 4] {comma, open, close, -}
+constexpr int kFWarpSmemHist = kFOffMB;
+constexpr int kFWarpSmemRec = kFOffMB + (kFWords + 4) * 16;
+static_assert(kFWarpSmemHist % 16 == 0 && kFWarpSmemRec % 16 == 0 && kFOffNlm % 16 == 0 && kFOffMA % 16 == 0 && kFOffP % 16 == 0 &&
+              kFOffInfo % 16 == 0 && kFOffMB % 16 == 0, "smem layout");
+
+enum { FK_BLANK = 0, FK_STMT, FK_LABEL, FK_DIR, FK_DECL, FK_OPEN, FK_CLOSE, FK_BAD };
+constexpr uint32_t kH80 = 0x80808080u;
+
+FFB_D uint32_t fk_pack(int kind, int b, int e) { return (uint32_t)b | ((uint32_t)e << 13) | ((uint32_t)kind << 26); }
+
+// bit 7 of every byte that DIFFERS from the replicated byte c4 (exact for 7-bit text; a byte
+// >= 0x80 may disturb its neighbour, such tiles are rejected before the masks are used)
+FFB_D uint32_t ne80(uint32_t w, uint32_t c4) { return (w ^ c4) + 0x7f7f7f7fu; }
+// four words of bit-7 flags -> 16 dense bits (bit 4j+k <-> byte k of word j)
+FFB_D uint32_t pack16(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+  const uint32_t q01 = (m0 >> 7) | (m1 >> 3), q23 = (m2 >> 7) | (m3 >> 3);
+  return ((q01 * 0x01020408u) >> 24) | (((q23 * 0x01020408u) >> 16) & 0xff00u);
+}
+
+// number of ';' (low half) and rare bytes (high half) at tile positions < x
+FFB_D uint32_t rank2(const uint4* MA, const uint32_t* P, int x) {
+  const int w = x >> 5;
+  const uint32_t low = (1u << (x & 31)) - 1u;
+  const uint2 m = *reinterpret_cast<const uint2*>(MA + w);
+  return P[w] + (uint32_t)__popc(m.x & low) + ((uint32_t)__popc(m.y & low) << 16);
+}
+
+// ---- bit-window statement parser ----------------------------------------------------------------
+// A statement of at most 64 bytes is parsed from 64-bit windows of the tile masks: bit i of a
+// window is the class of byte kb + i.  Everything the windows cannot express exactly (longer
+// statements, nested brackets, empty operands, odd predicates) returns false and goes through
+// do_statement, the byte-serial walk shared with the exact kernel.
+FFB_D uint64_t win64(uint32_t a, uint32_t b, uint32_t c, int sh) {
+  return (uint64_t)__funnelshift_r(a, b, sh) | ((uint64_t)__funnelshift_r(b, c, sh) << 32);
+}
+FFB_D uint64_t low_mask(int n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }      // bits [0, n)
+FFB_D uint64_t high_mask(int n) { return n >= 64 ? 0ull : (~0ull << n); }              // bits [n, 64)
+FFB_D uint64_t prefix_xor64(uint64_t x) {
+  x ^= x << 1; x ^= x << 2; x ^= x << 4; x ^= x << 8; x ^= x << 16; x ^= x << 32;
+  return x;
+}
+// s[p, p+len) as a little-endian u64, len <= 8 (three aligned word loads, no byte loop)
+FFB_D uint64_t load_packed(const uint8_t* s, int p, int len) {
+  if (len <= 0) return 0ull;
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + (p & ~3));
+  const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+  const int sh = (p & 3) * 8;
+  uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+  if (len <= 4) { hi = 0u; lo &= 0xffffffffu >> (32 - 8 * len); }
+  else hi &= 0xffffffffu >> (64 - 8 * len);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+// ---- cold paths, kept OUT of line -----------------------------------------------------------------
+// The hot loop has to fit the instruction cache (the first version of this kernel inlined every
+// byte-serial helper several times, grew to 17 K instructions and spent 80% of its issue slots
+// waiting for instruction fetch, ncu r1l).  Everything rare is a real call: arguments by value,
+// results in registers, so that no hot variable is forced into local memory.
+#define FFB_NOINLINE __device__ __noinline__
+FFB_NOINLINE uint64_t cold_norm_hash(const uint8_t* s, int a, int b) { return norm_hash(s, a, b); }
+FFB_NOINLINE uint64_t cold_describe_operand(const uint8_t* s, int a, int b) { return describe_operand(s, a, b); }
+struct AddrDesc { uint64_t desc; uint32_t kind; };
+FFB_NOINLINE AddrDesc cold_describe_address(const uint8_t* s, int a, int b) {
+  AddrDesc r;
+  r.kind = describe_address(s, a, b, &r.desc);
+  return r;
+}
+struct DeclResult { unsigned long long regs, shared; int n_reg_decl; };
+FFB_NOINLINE DeclResult cold_directive(const uint8_t* s, int b, int e) {
+  DeclResult r;
+  r.regs = 0; r.shared = 0; r.n_reg_decl = 0;
+  while (e > b && ffb_is_ws(s[e - 1])) --e;
+  uint64_t n = 0, bytes = 0;
+  int c0 = 0, c1 = 0;
+  if (parse_reg_decl(s, b, e, &n, &c0, &c1)) { r.regs = n; r.n_reg_decl = 1; }
+  else if (parse_shared_decl(s, b, e, &bytes)) r.shared = bytes;
+  return r;
+}
+// the byte-serial statement walk of the exact kernel; returns the opcode class
+template <int kMode>
+FFB_NOINLINE uint32_t cold_statement(const LexArgs* a, const uint64_t* tok_key, const uint32_t* tok_val, const uint8_t* cls,
+                                     const uint8_t* s, int kb, int ke, long long ins_at, long long ins_limit, uint32_t line,
+                                     long long abase, long long seg_begin) {
+  Emit em;
+  em.a = a; em.seg = 0; em.seg_begin = seg_begin; em.abase = abase; em.line = line;
+  em.tok.key = tok_key; em.tok.val = tok_val; em.cls = cls;
+  em.ins_at = ins_at; em.lab_at = 0; em.ins_limit = ins_limit; em.lab_limit = 0; em.dcl_at = 0;
+  em.c0 = em.c1 = em.c2 = 0; em.shared_bytes = 0; em.regs = 0;
+  do_statement<kMode>(s, kb, ke, em);
+  const uint64_t w = em.c0 ? em.c0 : (em.c1 ? em.c1 : em.c2);
+  return (em.c0 ? 0u : (em.c1 ? 3u : 6u)) + ((w >> 42) ? 2u : ((w >> 21) ? 1u : 0u));
+}
+
+// s[p, p+len) as two little-endian u64, 1 <= len <= 16 (five aligned word loads)
+FFB_D void load_packed16(const uint8_t* s, int p, int len, uint64_t* lo, uint64_t* hi) {
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + (p & ~3));
+  const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4];
+  const int sh = (p & 3) * 8;
+  const uint64_t l = (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
+  const uint64_t h = (uint64_t)__funnelshift_r(w2, w3, sh) | ((uint64_t)__funnelshift_r(w3, w4, sh) << 32);
+  if (len <= 8) { *lo = l & low_mask(8 * len); *hi = 0ull; }
+  else { *lo = l; *hi = h & low_mask(8 * (len - 8)); }
+}
+// the last k (<= 8) bytes of the first `len` (>= k) bytes of the packed pair
+FFB_D uint64_t packed_tail(uint64_t lo, uint64_t hi, int len, int k) {
+  const int sh = 8 * (len - k);
+  const uint64_t v = sh == 0 ? lo : (sh >= 64 ? hi >> (sh - 64) : (lo >> sh) | (hi << (64 - sh)));
+  return v & low_mask(8 * k);
+}
+FFB_D uint64_t hash_span(const uint8_t* s, int a, int b) {      // norm_hash of a span without newlines
+  if (b - a > 16 || b <= a) return cold_norm_hash(s, a, b);
+  uint64_t lo, hi;
+  load_packed16(s, a, b - a, &lo, &hi);
+  return ffb_hash_packed(lo, hi, (uint32_t)(b - a));
+}
+
+// describe_operand (alignment.py:31-47, cfg.py:184-188) for operands of at most 16 bytes, from two
+// packed words: same descriptor, no byte loops.  The few shapes that need Python's full int(text, 0)
+// grammar (prefixed or '_'-separated literals) and longer operands use describe_operand itself.
+FFB_D uint64_t describe_fast(const uint8_t* s, int a, int b) {
+  const int len = b - a;
+  if (len > 16) return cold_describe_operand(s, a, b);
+  uint64_t lo, hi;
+  load_packed16(s, a, len, &lo, &hi);
+  const uint64_t h = ffb_hash_packed(lo, hi, (uint32_t)len);
+  const unsigned c0 = (unsigned)(lo & 0xffu);
+  if (c0 == '%') {
+    if (len == 6 && lo == ffb_pk("%tid.x")) return ffb_op_make(FFB_OPK_TIDX, h);
+    if ((len >= 5 && (lo & 0xffffffffffull) == ffb_pk("%tid.")) || (len == 7 && (lo == ffb_pk("%laneid") || lo == ffb_pk("%warpid"))))
+      return ffb_op_make(FFB_OPK_UNKNOWN, h);
+    bool uni = false;
+    if (len >= 7) {
+      const uint64_t t7 = packed_tail(lo, hi, len, 7);
+      uni = t7 == ffb_pk("%gridid") || t7 == ffb_pk("WARP_SZ");
+    }
+    if (!uni && len >= 2) {
+      const uint64_t t2 = packed_tail(lo, hi, len, 2);
+      const unsigned ax = (unsigned)(t2 >> 8);
+      if ((t2 & 0xffu) == '.' && (ax == 'x' || ax == 'y' || ax == 'z')) {
+        const int L = len - 2;
+        uni = (L >= 6 && packed_tail(lo, hi, L, 6) == ffb_pk("%ctaid")) || (L >= 7 && packed_tail(lo, hi, L, 7) == ffb_pk("%nctaid")) ||
+              (L >= 5 && packed_tail(lo, hi, L, 5) == ffb_pk("%ntid"));
+      }
+    }
+    return ffb_op_make(uni ? FFB_OPK_UNIFORM_REG : FFB_OPK_REG, h);
+  }
+  // Python int(text, 0)
+  const bool sign = c0 == '+' || c0 == '-';
+  const int m = len - (sign ? 1 : 0);
+  if (m <= 0) return ffb_op_make(FFB_OPK_UNIFORM, h);
+  uint64_t dl = lo, dh = hi;
+  if (sign) { dl = (lo >> 8) | (hi << 56); dh = hi >> 8; }
+  const unsigned d0 = (unsigned)(dl & 0xffu);
+  if (!ffb_is_digit(d0)) return ffb_op_make(FFB_OPK_UNIFORM, h);
+  constexpr uint64_t k30 = 0x3030303030303030ull, k76 = 0x7676767676767676ull, k80 = 0x8080808080808080ull,
+                     k5f = 0x5f5f5f5f5f5f5f5full, k7f = 0x7f7f7f7f7f7f7f7full;
+  const uint64_t pl = dl | (k30 & ~low_mask(8 * (m < 8 ? m : 8))), ph = dh | (k30 & ~low_mask(8 * (m > 8 ? m - 8 : 0)));
+  const uint64_t nd = ((((pl ^ k30) + k76) | ((ph ^ k30) + k76)) | pl | ph) & k80;          // some byte is not 0-9
+  if (nd) {
+    const uint64_t other = (((pl ^ k30) + k76) & ((pl ^ k5f) + k7f)) | (((ph ^ k30) + k76) & ((ph ^ k5f) + k7f)) | pl | ph;
+    const unsigned d1 = (unsigned)((dl >> 8) & 0xffu) | 32u;
+    const bool prefixed = d0 == '0' && m >= 2 && (d1 == 'x' || d1 == 'o' || d1 == 'b');
+    if (prefixed || !(other & k80)) return cold_describe_operand(s, a, b);    // 0x.. / 0o.. / 0b.. or digits with '_'
+    return ffb_op_make(FFB_OPK_UNIFORM, h);                                // base 10 meets a foreign byte: not a literal
+  }
+  uint64_t v = 0;
+  bool nonzero = false;
+#pragma unroll 1
+  for (int k = 0; k < m; ++k) {
+    const unsigned d = (unsigned)(((k < 8 ? dl >> (8 * k) : dh >> (8 * (k - 8)))) & 0xfu);
+    nonzero = nonzero || d != 0;
+    v = v * 10u + d;
+  }
+  if (d0 == '0' && nonzero) return ffb_op_make(FFB_OPK_UNIFORM, h);       // "010": rejected by int(.., 0)
+  const int64_t sv = c0 == '-' ? -(int64_t)v : (int64_t)v;
+  return ffb_op_make(FFB_OPK_INT, (uint64_t)sv);
+}
+
+// describe_address (alignment.py:21) for the canonical shapes `[base]`, `[base+N]`, `[base+-N]` of at
+// most 16 bytes without blanks or inner brackets (the caller checks those on the mask windows and
+// that the operand starts with '[').  Returns false for anything else: the byte-serial version decides.
+FFB_D bool address_fast(const uint8_t* s, int a, int b, uint32_t* kind, uint64_t* desc) {
+  const int len = b - a;
+  uint64_t lo, hi;
+  load_packed16(s, a, len, &lo, &hi);
+  if (packed_tail(lo, hi, len, 1) != ']') return false;
+  constexpr uint64_t k80 = 0x8080808080808080ull, k7f = 0x7f7f7f7f7f7f7f7full, k2b = 0x2b2b2b2b2b2b2b2bull,
+                     k30 = 0x3030303030303030ull, k76 = 0x7676767676767676ull;
+  const uint64_t pl = ~((lo ^ k2b) + k7f) & k80, ph = ~((hi ^ k2b) + k7f) & k80;      // '+' bytes
+  int plus = -1;
+  if (pl) plus = (__ffsll((long long)pl) - 1) >> 3; else if (ph) plus = 8 + ((__ffsll((long long)ph) - 1) >> 3);
+  const int base_end = plus >= 0 ? plus : len - 1;
+  *desc = 0;
+  if (base_end <= 1) { *kind = FFB_ADDR_NOMATCH; return true; }          // empty base
+  if (plus >= 0) {                                                       // `+ -? digits` up to the bracket
+    int d0 = plus + 1;
+    const int sh0 = 8 * d0;
+    const unsigned c = (unsigned)((sh0 >= 64 ? hi >> (sh0 - 64) : lo >> sh0) & 0xffu);
+    if (c == '-') ++d0;
+    const int m = len - 1 - d0;
+    if (m <= 0) { *kind = FFB_ADDR_NOMATCH; return true; }
+    const int sh = 8 * d0;                                               // digits start at byte d0 (1..15)
+    const uint64_t dl = sh >= 64 ? hi >> (sh - 64) : (lo >> sh) | (hi << (64 - sh)), dh = sh >= 64 ? 0ull : hi >> sh;
+    const uint64_t ml = low_mask(8 * (m < 8 ? m : 8)), mh = low_mask(8 * (m > 8 ? m - 8 : 0));
+    const uint64_t ql = (dl & ml) | (k30 & ~ml), qh = (dh & mh) | (k30 & ~mh);
+    if (((((ql ^ k30) + k76) | ((qh ^ k30) + k76)) | ql | qh) & k80) { *kind = FFB_ADDR_NOMATCH; return true; }
+  }
+  if (((lo >> 8) & 0xffu) != '%') { *kind = FFB_ADDR_SYMBOL; return true; }
+  const int blen = base_end - 1;
+  uint64_t bl = (lo >> 8) | (hi << 56), bh = hi >> 8;
+  if (blen <= 8) { bl &= low_mask(8 * blen); bh = 0ull; } else bh &= low_mask(8 * (blen - 8));
+  *desc = ffb_op_make(FFB_OPK_REG, ffb_hash_packed(bl, bh, (uint32_t)blen));
+  *kind = FFB_ADDR_REG;
+  return true;
+}
+
+template <int kMode>
+FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, int kb, int ke, Emit& em) {
+  const int n = ke - kb;
+  if (kMode == 2 && n > 64) return false;
+  const int w0 = kb >> 5, sh = kb & 31;
+  const uint64_t valid = low_mask(n);
+  uint64_t BL, DT;
+  {
+    const uint4 a0 = MA[w0], a1 = MA[w0 + 1], a2 = MA[w0 + 2];
+    BL = win64(a0.z, a1.z, a2.z, sh) & valid;
+    DT = win64(a0.w, a1.w, a2.w, sh) & valid;
+  }
+  // ---- predicate  ^@(!?%[\w$]+)\s+  (ptx.py:42) ----
+  int o0 = 0, p0 = 0, p1 = 0;
+  bool has_pred = false, neg = false;
+  if (s[kb] == '@') {
+    if (!BL) return false;
+    const int t1 = __ffsll((long long)BL) - 1;
+    int j = kb + 1;
+    neg = s[j] == '!';
+    if (neg) ++j;
+    if (s[j] != '%' || kb + t1 <= j + 1) return false;
+#pragma unroll 1
+    for (int k = j + 1; k < kb + t1; ++k)
+      if (!ffb_is_name_char(s[k])) return false;
+    const uint64_t rest = ~BL & valid & high_mask(t1);
+    if (!rest) return false;
+    has_pred = true; p0 = j; p1 = kb + t1;
+    o0 = __ffsll((long long)rest) - 1;
+  }
+  // ---- opcode tokens (ptx.py:99-136, :64-76) ----
+  const uint64_t after = BL & high_mask(o0);
+  if (!after && n > 64) return false;
+  const int o1 = after ? __ffsll((long long)after) - 1 : n;
+  uint64_t D = DT & low_mask(o1) & high_mask(o0);
+  uint32_t base = TB_NONE, elem_code = 0, vec = 0, space = 0, cmp = 0, flags = 0;
+  {
+    int ts = o0, ti = 0;
+    for (;;) {
+      const int te = D ? __ffsll((long long)D) - 1 : o1;
+      const int len = te - ts;
+      const uint32_t v = len > 8 ? 0u : tok_lookup(em.tok, load_packed(s, kb + ts, len));
+      flags &= ~8u;
+      if (ti == 0) base = v & 31u;
+      else {
+        const uint32_t ec = (v >> 5) & 7u;
+        if (ec) elem_code = ec;
+        flags |= (v >> 8) & 3u;
+        const uint32_t vc = (v >> 10) & 3u;
+        if (vc) vec = vc;
+        if (v & (1u << 12)) flags |= 8u;
+        const uint32_t sp = (v >> 13) & 7u;
+        if (sp && !space) space = sp;
+      }
+      if (v & (1u << 16)) flags |= 4u;
+      if (!cmp) cmp = (v >> 17) & 7u;
+      if (!D) break;
+      D &= D - 1;
+      ts = te + 1; ++ti;
+    }
+  }
+  const OpcodeInfo oc = finish_opcode(base, elem_code, vec, space, cmp, flags);
+  if (kMode == 2) {
+    // ---- operands: top-level commas (ptx.py:144-162) ----
+    uint64_t CM, OP, CL;
+    {
+      const uint4 b0 = MB[w0], b1 = MB[w0 + 1], b2 = MB[w0 + 2];
+      CM = win64(b0.x, b1.x, b2.x, sh); OP = win64(b0.y, b1.y, b2.y, sh); CL = win64(b0.z, b1.z, b2.z, sh);
+    }
+    const uint64_t R = valid & high_mask(o1);
+    const uint64_t NB = ~BL & R;
+    OP &= R; CL &= R;
+    uint64_t inside = 0;
+    if (OP | CL) {                                    // brackets must alternate open / close (depth 0 or 1)
+      const uint64_t X = OP | CL, incl = prefix_xor64(X), excl = incl ^ X;
+      if ((OP & excl) || (CL & ~excl) || (__popcll(X) & 1)) return false;
+      inside = incl;
+    }
+    const uint64_t C0 = CM & R & ~inside;
+    const bool is_mem = oc.cls == FFB_CLS_MEMLOAD || oc.cls == FFB_CLS_MEMSTORE;
+    const bool aux_is_op4 = !is_mem && oc.cls != FFB_CLS_BRANCH;
+    FfbInsRec rec;
+    rec.op[0] = rec.op[1] = rec.op[2] = rec.op[3] = 0; rec.aux = 0;
+    int count = 0, as = -1, ae = -1, last_s = -1, last_e = -1;
+    bool extra_reg = false, dst_reg = false;
+    {
+      uint64_t rem = C0;
+      int from = o1;
+      for (;;) {
+        const int to = rem ? __ffsll((long long)rem) - 1 : n;
+        const uint64_t seg = NB & low_mask(to) & high_mask(from);
+        if (!seg) {
+          if (C0) return false;                       // empty operand between commas: the walk drops it
+          break;
+        }
+        const int a = kb + __ffsll((long long)seg) - 1, b = kb + 64 - __clzll((long long)seg);
+        const unsigned c_first = s[a];
+        if (count == 0) dst_reg = c_first == '%';
+        if (count < 4 || (count == 4 && aux_is_op4)) {
+          const uint64_t d = describe_fast(s, a, b);
+          if (count == 0) rec.op[0] = d; else if (count == 1) rec.op[1] = d; else if (count == 2) rec.op[2] = d;
+          else if (count == 3) rec.op[3] = d; else rec.aux = d;
+        } else if (c_first == '%') extra_reg = true;
+        if (is_mem && as < 0 && c_first == '[') { as = a; ae = b; }
+        last_s = a; last_e = b;
+        ++count;
+        if (!rem) break;
+        rem &= rem - 1;
+        from = to + 1;
+      }
+    }
+    uint32_t addr_kind = FFB_ADDR_ABSENT;
+    if (is_mem) {
+      if (as >= 0) {
+        const uint64_t span = low_mask(ae - kb) & high_mask(as - kb);
+        const bool canonical = ae - as <= 16 && !(BL & span) && ((OP | CL) & span) == ((1ull << (as - kb)) | (1ull << (ae - kb - 1)));
+        if (!canonical || !address_fast(s, as, ae, &addr_kind, &rec.aux)) {
+          const AddrDesc ad = cold_describe_address(s, as, ae);
+          addr_kind = ad.kind; rec.aux = ad.desc;
+        }
+      }
+    }
+    else if (!aux_is_op4) rec.aux = last_s >= 0 ? ffb_op_make(FFB_OPK_REG, hash_span(s, last_s, last_e)) : 0ull;
+    rec.line = em.line;
+    rec.off = (uint32_t)(em.abase + kb - em.seg_begin);
+    rec.len = (uint32_t)(64 - __clzll((long long)(~BL & valid)));
+    rec.pred = has_pred ? hash_span(s, p0, p1) : 0ull;
+    rec.meta = oc.cls | (oc.space << 4) | ((oc.bytes & 63u) << 7) | (oc.base << 13) | ((has_pred ? 1u : 0u) << 18) |
+               ((neg ? 1u : 0u) << 19) | ((uint32_t)(count > 7 ? 7 : count) << 20) | (oc.cmp << 23) | (addr_kind << 26) |
+               ((dst_reg ? 1u : 0u) << 28) | ((extra_reg ? 1u : 0u) << 29);
+    if (em.ins_at < em.ins_limit) {
+      em.a->ins[em.ins_at] = rec;
+      if (em.a->meta) em.a->meta[em.ins_at] = rec.meta;
+    }
+  }
+  const uint64_t inc = 1ull << (21 * (oc.cls % 3u));
+  em.c0 += oc.cls < 3u ? inc : 0ull; em.c1 += (oc.cls >= 3u && oc.cls < 6u) ? inc : 0ull; em.c2 += oc.cls >= 6u ? inc : 0ull;
+  return true;
+}
+
+// A line without rare bytes, or what is left of a careful one: s[b,e) holds no ':' and no
+// comment; braces, if any, are balanced.  nsemi = number of ';' in it.
+FFB_D int classify_plain(const uint8_t* s, int b, int e, int nsemi, int* kb, int* ke) {
+  int fb = b;
+#pragma unroll 1
+  while (fb < e && s[fb] <= ' ') ++fb;
+  if (fb >= e) return FK_BLANK;
+  int lb = e - 1;
+#pragma unroll 1
+  while (s[lb] <= ' ') --lb;
+  const unsigned c0 = s[fb];
+  *kb = fb;
+  if (c0 == '.') {                                               // ptx.py:240-256
+    if (nsemi == 0) *ke = lb + 1;
+    else if (nsemi == 1 && s[lb] == ';') *ke = lb;
+    else return FK_BAD;                                          // text behind the first ';'
+    const bool decl = (s[fb + 1] == 'r' && s[fb + 2] == 'e' && s[fb + 3] == 'g') ||
+                      (s[fb + 1] == 's' && s[fb + 2] == 'h' && s[fb + 3] == 'a');
+    return decl ? FK_DECL : FK_DIR;
+  }
+  if (nsemi != 1 || s[lb] != ';') return FK_BAD;                 // pending / several statements
+  if (lb == fb) return FK_BLANK;                                 // a lone ';' (ptx.py:268-269)
+  *ke = lb;
+  return FK_STMT;
+}
+
+// A line with rare bytes.  s[b,e) is the raw line (scanned whole for "/*"), classification
+// starts at bc >= b (the byte after the kernel's opening brace on that one line).
+FFB_D int resolve_careful(const uint8_t* s, int b, int bc, int e, int* kb, int* ke, bool* slashstar) {
+  int cut = e, ncolon = 0, colon_at = -1, nsemi = 0, run = 0, minrun = 0, nbrace = 0;
+  bool ss = false;
+#pragma unroll 1
+  for (int i = b; i < e; ++i) {
+    const unsigned c = s[i];
+    if (c == '/') {
+      const unsigned c2 = s[i + 1];
+      if (c2 == '*') ss = true;
+      else if (c2 == '/' && cut == e) cut = i;
+    }
+    if (i >= bc && i < cut) {
+      if (c == ';') ++nsemi;
+      else if (c == ':') { if (ncolon++ == 0) colon_at = i; }
+      else if (c == '{') { ++run; ++nbrace; }
+      else if (c == '}') { --run; ++nbrace; if (run < minrun) minrun = run; }
+    }
+  }
+  *slashstar = ss;
+  int fb = bc;
+#pragma unroll 1
+  while (fb < cut && s[fb] <= ' ') ++fb;
+  if (fb >= cut) return FK_BLANK;
+  int lb = cut - 1;
+#pragma unroll 1
+  while (s[lb] <= ' ') --lb;
+  *kb = fb;
+  if (ncolon) {                                                  // ptx.py:232-236, label alone on its line
+    if (ncolon != 1 || colon_at != lb || lb == fb) return FK_BAD;
+#pragma unroll 1
+    for (int i = fb; i < lb; ++i)
+      if (!ffb_is_label_char(s[i])) return FK_BAD;
+    *ke = lb;
+    return FK_LABEL;
+  }
+  if (nbrace) {
+    if (fb == lb) return s[fb] == '{' ? FK_OPEN : FK_CLOSE;      // ptx.py:237-239
+    if (run != 0 || minrun < 0) return FK_BAD;
+  }
+  return classify_plain(s, fb, cut, nsemi, kb, ke);
+}
+
+// first set bit of the lane's four mask words at tile position >= from (and < lim) for which
+// pred(pos) holds; 0x7fffffff if none
+template <typename Pred>
+FFB_D int lane_first(const uint32_t w[4], int lane, int from, int lim, Pred pred) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int base = lane * 128 + 32 * k;
+    if (from >= base + 32) continue;
+    uint32_t m = w[k];
+    if (from > base) m &= 0xffffffffu << (from - base);
+    while (m) {
+      const int pos = base + __ffs((int)m) - 1;
+      m &= m - 1;
+      if (pos >= lim) return 0x7fffffff;
+      if (pred(pos)) return pos;
+    }
+  }
+  return 0x7fffffff;
+}
+
+FFB_D bool in_line_comment(const uint8_t* s, int at, int lo) {   // is a "//" open between the line start and `at`?
+  for (int i = at - 2; i >= lo && s[i] != '\n'; --i)
+    if (s[i] == '/' && s[i + 1] == '/') return true;
+  return false;
+}
+
+template <bool kRecords>
+__global__ void __launch_bounds__(kFWarps * 32, kRecords ? 4 : 6)
+lex_fast_kernel(LexArgs a) {
+  constexpr int kMain = kRecords ? 2 : 1;
+  FFB_DYN_SMEM(smem_raw);
+  __shared__ uint8_t s_cls[256];
+  __shared__ uint64_t s_tok_key[256];
+  __shared__ uint32_t s_tok_val[256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint8_t* s = smem_raw + (size_t)wid * (kRecords ? kFWarpSmemRec : kFWarpSmemHist);
+  uint32_t* NLM = reinterpret_cast<uint32_t*>(s + kFOffNlm);
+  uint16_t* clist = reinterpret_cast<uint16_t*>(s + kFOffNlm);
+  uint4* MA = reinterpret_cast<uint4*>(s + kFOffMA);
+  uint4* MB = reinterpret_cast<uint4*>(s + kFOffMB);
+  uint32_t* P = reinterpret_cast<uint32_t*>(s + kFOffP);
+  uint16_t* nl = reinterpret_cast<uint16_t*>(s + kFOffNl);
+  uint32_t* linfo = reinterpret_cast<uint32_t*>(s + kFOffInfo);
+  for (int c = threadIdx.x; c < 256; c += kFWarps * 32) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kNumTokDefs; c += kFWarps * 32) {
+    const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
+    s_tok_key[slot] = kTokDefs[c].key; s_tok_val[slot] = kTokDefs[c].val;
+  }
+  for (int i = lane; i < kFPad; i += 32) s[kFTile + i] = '\n';      // never overwritten
+  if (lane < 4) {                                                   // windows and rank2(kFTile) read past the last word
+    MA[kFWords + lane] = make_uint4(0u, 0u, 0u, 0u);
+    if (kRecords) MB[kFWords + lane] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncthreads();
+
+  for (;;) {
+    unsigned long long wq = 0;
+    if (lane == 0) wq = atomicAdd(a.work, 1ull);
+    wq = __shfl_sync(kFull, wq, 0);
+    if (wq >= (unsigned long long)a.n_segs) break;
+    const int64_t seg = a.order ? (int64_t)a.order[wq] : (int64_t)wq;
+    const int64_t seg_begin = a.seg_off[seg], seg_end = a.seg_off[seg + 1];
+
+    int phase = PH_SEARCH, depth = 0;
+    bool reject = false;
+    uint32_t line_no = 1;
+    int64_t cur = seg_begin, scan_from_g = seg_begin, body_pos_g = 0;
+    int64_t name_off = 0, name_len = 0, body_end_off = 0;
+    uint32_t n_instr = 0, n_labels = 0, n_decls = 0, n_slow_seg = 0;
+    const int64_t ins_base = kRecords ? a.ins_base[seg] : 0, lab_base = kRecords ? a.lab_base[seg] : 0;
+
+    Emit em;
+    em.a = &a; em.seg = seg; em.seg_begin = seg_begin; em.abase = 0; em.line = 0;
+    em.tok.key = s_tok_key; em.tok.val = s_tok_val; em.cls = s_cls;
+    em.ins_at = ins_base; em.lab_at = lab_base;
+    em.ins_limit = (kRecords && a.ins_cap) ? ins_base + a.ins_cap[seg] : 0x7fffffffffffffffLL;
+    em.lab_limit = (kRecords && a.lab_cap) ? lab_base + a.lab_cap[seg] : 0x7fffffffffffffffLL;
+    em.dcl_at = 0;
+    em.c0 = em.c1 = em.c2 = 0;
+    em.shared_bytes = 0; em.regs = 0;
+
+    while (phase != PH_DONE && cur < seg_end) {
+      const int64_t abase = cur & ~(int64_t)15;
+      const int64_t hi_g = (abase + kFTile < seg_end) ? abase + kFTile : seg_end;
+      const int lo = (int)(cur - abase), hi = (int)(hi_g - abase);
+      const bool at_seg_end = hi_g == seg_end;
+      em.abase = abase;
+      __syncwarp();
+
+      // ================= M: load, masks, stage =================
+      uint32_t badacc = 0;
+#pragma unroll 1
+      for (int v0 = 0; v0 < 8; v0 += 2) {                        // rolled on purpose: code size (see the note on cold paths)
+        uint4 q[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int64_t g = abase + (int64_t)((v0 + v) * 32 + lane) * 16;
+          if (g + 16 <= a.n_bytes && g < hi_g) q[v] = *reinterpret_cast<const uint4*>(a.text + g);
+          else q[v].x = q[v].y = q[v].z = q[v].w = 0x0a0a0a0au;
+        }
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int u = (v0 + v) * 32 + lane, us = u * 16;
+          uint32_t w[4] = {q[v].x, q[v].y, q[v].z, q[v].w};
+          uint32_t keep = 0xffffu;
+          if (us < lo || us + 16 > hi) {                         // unit straddles the tile's live range
+            keep = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int p = us + 4 * j + k;
+                if (p >= lo && p < hi) keep |= 1u << (4 * j + k);
+                else w[j] = (w[j] & ~(0xffu << (8 * k))) | (0x0au << (8 * k));
+              }
+          }
+          uint32_t n80[4], s80[4], r80[4], d80[4], b80[4], c80[4], o80[4], l80[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t x = w[j];
+            const uint32_t tn = ne80(x, 0x0a0a0a0au), tt = ne80(x, 0x09090909u);
+            n80[j] = ~tn & kH80;
+            s80[j] = ~ne80(x, 0x3b3b3b3bu) & kH80;
+            r80[j] = ~(ne80(x, 0x3a3a3a3au) & ne80(x, 0x7b7b7b7bu) & ne80(x, 0x7d7d7d7du) & ne80(x, 0x2f2f2f2fu)) & kH80;
+            b80[j] = ~(tt & ne80(x, 0x20202020u)) & kH80;
+            d80[j] = ~ne80(x, 0x2e2e2e2eu) & kH80;
+            if (kRecords) {
+              const uint32_t y = x | 0x20202020u;              // '[' -> '{', ']' -> '}'
+              c80[j] = ~ne80(x, 0x2c2c2c2cu) & kH80;
+              o80[j] = ~(ne80(y, 0x7b7b7b7bu) & ne80(x, 0x28282828u)) & kH80;
+              l80[j] = ~(ne80(y, 0x7d7d7d7du) & ne80(x, 0x29292929u)) & kH80;
+            }
+            // bytes >= 0x80, and control bytes other than \t \n
+            badacc |= (x & kH80) | (~(x + 0x60606060u) & kH80 & tn & tt);
+          }
+          *reinterpret_cast<uint4*>(s + us) = make_uint4(w[0], w[1], w[2], w[3]);
+          reinterpret_cast<uint16_t*>(NLM)[u] = (uint16_t)(pack16(n80[0], n80[1], n80[2], n80[3]) & keep);
+          uint16_t* m16 = reinterpret_cast<uint16_t*>(MA + (u >> 1)) + (u & 1);     // field f of word u/2: halfword 2f + (u&1)
+          m16[0] = (uint16_t)pack16(s80[0], s80[1], s80[2], s80[3]);
+          m16[2] = (uint16_t)pack16(r80[0], r80[1], r80[2], r80[3]);
+          m16[4] = (uint16_t)pack16(b80[0], b80[1], b80[2], b80[3]);
+          m16[6] = (uint16_t)pack16(d80[0], d80[1], d80[2], d80[3]);
+          if (kRecords) {
+            uint16_t* x16 = reinterpret_cast<uint16_t*>(MB + (u >> 1)) + (u & 1);
+            x16[0] = (uint16_t)pack16(c80[0], c80[1], c80[2], c80[3]);
+            x16[2] = (uint16_t)pack16(o80[0], o80[1], o80[2], o80[3]);
+            x16[4] = (uint16_t)pack16(l80[0], l80[1], l80[2], l80[3]);
+          }
+        }
+      }
+      __syncwarp();
+      if (__any_sync(kFull, badacc != 0)) { reject = true; break; }
+
+      // ================= T: line table and prefix counts =================
+      uint32_t rw[4], dw[4];                                     // this lane's rare / dot words (S phase)
+      int total_nl = 0;
+      {
+        const uint4 nw = *reinterpret_cast<const uint4*>(NLM + 4 * lane);
+        const uint4 m0 = MA[4 * lane], m1 = MA[4 * lane + 1], m2 = MA[4 * lane + 2], m3 = MA[4 * lane + 3];
+        rw[0] = m0.y; rw[1] = m1.y; rw[2] = m2.y; rw[3] = m3.y;
+        dw[0] = m0.w; dw[1] = m1.w; dw[2] = m2.w; dw[3] = m3.w;
+        const uint32_t c0 = (uint32_t)__popc(m0.x) | ((uint32_t)__popc(m0.y) << 16);
+        const uint32_t c1 = (uint32_t)__popc(m1.x) | ((uint32_t)__popc(m1.y) << 16);
+        const uint32_t c2 = (uint32_t)__popc(m2.x) | ((uint32_t)__popc(m2.y) << 16);
+        const uint32_t c3 = (uint32_t)__popc(m3.x) | ((uint32_t)__popc(m3.y) << 16);
+        int tot_sr = 0;
+        const uint32_t ex = (uint32_t)warp_excl_sum((int)(c0 + c1 + c2 + c3), &tot_sr);
+        *reinterpret_cast<uint4*>(P + 4 * lane) = make_uint4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
+        if (lane == 31) P[kFWords] = (uint32_t)tot_sr;
+        const uint32_t nwv[4] = {nw.x, nw.y, nw.z, nw.w};
+        int at = warp_excl_sum(__popc(nw.x) + __popc(nw.y) + __popc(nw.z) + __popc(nw.w), &total_nl);
+        __syncwarp();                                            // NLM fully read before it becomes the careful list
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t m = nwv[k];
+          while (m) {
+            const int bit = __ffs((int)m) - 1;
+            m &= m - 1;
+            if (at < kFMaxLines) nl[at] = (uint16_t)(lane * 128 + 32 * k + bit);
+            ++at;
+          }
+        }
+      }
+      const int n_real = total_nl < kFMaxLines ? total_nl : kFMaxLines;
+      const bool virtual_last = at_seg_end && total_nl < kFMaxLines;   // text may end without a newline
+      if (virtual_last && lane == 0) nl[n_real] = (uint16_t)hi;
+      const int n_lines = n_real + (virtual_last ? 1 : 0);
+      __syncwarp();
+      if (n_lines == 0) { reject = true; break; }                // a line longer than the tile
+      const int region_end = virtual_last ? hi : nl[n_real - 1] + 1;
+
+      // ================= S: kernel header (ptx.py:165-176) =================
+      if (phase == PH_SEARCH) {
+        int from = (int)(scan_from_g - abase);
+        if (from < lo) from = lo;
+        for (;;) {
+          int cand = lane_first(dw, lane, from, region_end, [&](int p) {
+            return s[p + 1] == 'e' && s[p + 2] == 'n' && s[p + 3] == 't' && s[p + 4] == 'r' && s[p + 5] == 'y'; });
+          cand = warp_min(cand);
+          if (cand == 0x7fffffff) { scan_from_g = abase + region_end; break; }
+          if (in_line_comment(s, cand, lo)) { from = cand + 1; continue; }
+          int q = cand + 6;
+          while (q < region_end && s[q] <= ' ') ++q;
+          if (q >= region_end) {                                 // `\s+NAME` may continue in the next tile
+            if (!at_seg_end) reject = true; else scan_from_g = abase + region_end;
+            break;
+          }
+          if (s[q] == '/') { reject = true; break; }             // a comment inside the match: exact kernel
+          if (q == cand + 6 || !ffb_is_name_start(s[q])) { from = cand + 1; continue; }
+          int r = q + 1;
+          while (r < region_end && ffb_is_name_char(s[r])) ++r;
+          name_off = abase + q - seg_begin; name_len = r - q;
+          phase = PH_HEADER; scan_from_g = abase + r;
+          break;
+        }
+        if (reject) break;
+      }
+      if (phase == PH_HEADER) {
+        int from = (int)(scan_from_g - abase);
+        if (from < lo) from = lo;
+        for (;;) {
+          int cand = lane_first(rw, lane, from, region_end, [&](int p) { return s[p] == '{'; });
+          cand = warp_min(cand);
+          if (cand == 0x7fffffff) { if (scan_from_g < abase + region_end) scan_from_g = abase + region_end; break; }
+          if (in_line_comment(s, cand, lo)) { from = cand + 1; continue; }
+          phase = PH_BODY; depth = 1; body_pos_g = abase + cand + 1;
+          break;
+        }
+      }
+
+      // ================= P1: line kinds =================
+      int pos = 0x7fffffff, first = n_lines;                     // first body byte / line of this tile
+      if (phase == PH_BODY) {
+        pos = body_pos_g > cur ? (int)(body_pos_g - abase) : lo;
+        first = 0;
+        if (pos > lo) {
+          for (int l = lane; l < n_lines; l += 32) first += (nl[l] < pos) ? 1 : 0;
+          first = (int)warp_sum_u64((unsigned long long)first);
+        }
+      }
+      int n_car = 0, bad_line = 0x7fffffff, ss_line = 0x7fffffff;
+      for (int l0 = 0; l0 < n_lines; l0 += 32) {
+        const int li = l0 + lane;
+        const bool live = li < n_lines;
+        bool careful = false;
+        if (live) {
+          const int b = li == 0 ? lo : nl[li - 1] + 1, e = nl[li];
+          const uint32_t r = rank2(MA, P, e) - rank2(MA, P, b);
+          careful = (r >> 16) != 0 || (li == first && pos > b);
+          if (!careful && li >= first) {
+            int kb = 0, ke = 0;
+            const int kind = classify_plain(s, b, e, (int)(r & 0xffffu), &kb, &ke);
+            linfo[li] = fk_pack(kind, kb, ke);
+            if (kind == FK_BAD && li < bad_line) bad_line = li;
+          }
+        }
+        const unsigned cm = __ballot_sync(kFull, careful);
+        if (careful) clist[n_car + __popc(cm & lt_mask)] = (uint16_t)li;
+        n_car += __popc(cm);
+      }
+      __syncwarp();
+      int end_line = 0x7fffffff, close_at = 0;
+      for (int c0 = 0; c0 < n_car; c0 += 32) {
+        const int ci = c0 + lane;
+        const bool live = ci < n_car;
+        int li = 0x7fffffff, kind = FK_BLANK, kb = 0, ke = 0;
+        if (live) {
+          li = clist[ci];
+          const int b = li == 0 ? lo : nl[li - 1] + 1, e = nl[li];
+          const int bc = (li == first && pos > b) ? pos : b;
+          bool ss = false;
+          kind = resolve_careful(s, b, bc, e, &kb, &ke, &ss);
+          if (ss && li < ss_line) ss_line = li;
+          if (li >= first) {
+            linfo[li] = fk_pack(kind, kb, ke);
+            if (kind == FK_BAD && li < bad_line) bad_line = li;
+          } else kind = FK_BLANK;
+        }
+        if (end_line == 0x7fffffff) {                            // brace depth over the body lines, in order
+          const int delta = kind == FK_OPEN ? 1 : (kind == FK_CLOSE ? -1 : 0);
+          int tot = 0;
+          const int d_after = depth + warp_excl_sum(delta, &tot) + delta;
+          const unsigned closing = __ballot_sync(kFull, kind == FK_CLOSE && d_after == 0);
+          if (closing) {
+            const int src = __ffs((int)closing) - 1;
+            end_line = __shfl_sync(kFull, li, src);
+            close_at = __shfl_sync(kFull, kb, src);
+          } else depth += tot;
+        }
+      }
+      __syncwarp();
+      const int n_eff = end_line < n_lines ? end_line : n_lines;
+      bad_line = warp_min(bad_line);
+      ss_line = warp_min(ss_line);
+      if (bad_line < n_eff || ss_line < n_eff || (end_line != 0x7fffffff && ss_line <= end_line)) { reject = true; break; }
+
+      // ================= P2: statements, labels, declarations =================
+      const uint32_t tile_ins0 = n_instr;
+      int n_slow = 0;
+      uint16_t* slist = clist;                                   // the careful list is dead by now
+      for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
+        const int li = l0 + lane;
+        const bool live = li >= first && li < n_eff;
+        const uint32_t inf = live ? linfo[li] : 0u;
+        const int kind = (int)(inf >> 26), kb = (int)(inf & 0x1fffu), ke = (int)((inf >> 13) & 0x1fffu);
+        const unsigned stm = __ballot_sync(kFull, kind == FK_STMT);
+        const unsigned lbm = __ballot_sync(kFull, kind == FK_LABEL);
+        const unsigned dcm = __ballot_sync(kFull, kind == FK_DECL);
+        const int64_t my_ins = ins_base + n_instr + __popc(stm & lt_mask);
+        bool slow = false;
+        if (kind == FK_STMT) {
+          em.ins_at = my_ins;
+          em.line = line_no + (uint32_t)li;
+          slow = !fast_statement<kMain>(s, MA, MB, kb, ke, em);
+        }
+        const unsigned slm = __ballot_sync(kFull, slow);
+        if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | ((int)(my_ins - ins_base - tile_ins0) << 8));
+        n_slow += __popc(slm);
+        if (kRecords && kind == FK_LABEL) {
+          const int64_t slot = lab_base + n_labels + __popc(lbm & lt_mask);
+          FfbLabelRec L;
+          L.hash = hash_span(s, kb, ke); L.index = (uint32_t)(my_ins - ins_base);
+          L.off = (uint32_t)(abase + kb - seg_begin);
+          if (slot < em.lab_limit) a.labels[slot] = L;
+        }
+        int nd = 0;
+        if (dcm) {
+          if (kind == FK_DECL) {
+            const DeclResult dr = cold_directive(s, kb, ke);
+            em.regs += dr.regs; em.shared_bytes += dr.shared; nd = dr.n_reg_decl;
+          }
+          nd = (int)warp_sum_u64((unsigned long long)nd);
+        }
+        n_instr += (uint32_t)__popc(stm); n_labels += (uint32_t)__popc(lbm); n_decls += (uint32_t)nd;
+      }
+      __syncwarp();
+      n_slow_seg += (uint32_t)n_slow;
+      for (int i0 = 0; i0 < n_slow; i0 += 32) {                 // statements the windows could not express
+        const int i = i0 + lane;
+        if (i < n_slow) {
+          const unsigned ent = slist[i];
+          const int li = (int)(ent & 255u);
+          const uint32_t inf = linfo[li];
+          const uint32_t cls = cold_statement<kMain>(&a, s_tok_key, s_tok_val, s_cls, s, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu),
+                                                     ins_base + tile_ins0 + (ent >> 8), em.ins_limit, line_no + (uint32_t)li, abase, seg_begin);
+          const uint64_t inc = 1ull << (21 * (cls % 3u));
+          em.c0 += cls < 3u ? inc : 0ull; em.c1 += (cls >= 3u && cls < 6u) ? inc : 0ull; em.c2 += cls >= 6u ? inc : 0ull;
+        }
+      }
+      if (end_line != 0x7fffffff) {
+        phase = PH_DONE;
+        body_end_off = abase + close_at - seg_begin;
+        break;
+      }
+
+      // ================= advance =================
+      line_no += (uint32_t)n_real;
+      const int64_t next = abase + region_end;
+      if (next <= cur) { reject = true; break; }
+      cur = next;
+    }
+
+    // ================= segment epilogue =================
+    // only complete, well-formed kernels are finished here; every error status comes from the exact kernel
+    bool ok = !reject && phase == PH_DONE && n_instr > 0;
+    if (kRecords && ok && ((a.ins_cap && (int64_t)n_instr > a.ins_cap[seg]) || (a.lab_cap && (int64_t)n_labels > a.lab_cap[seg]))) ok = false;
+    if (!ok) {
+      if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1ull)] = (int32_t)seg;
+      continue;
+    }
+#pragma unroll 1
+    for (int c = 0; c < FFB_N_CLASSES; ++c) {
+      const uint64_t word = c < 3 ? em.c0 : (c < 6 ? em.c1 : em.c2);
+      const uint32_t tot = (uint32_t)warp_sum_u64((word >> (21 * (c % 3))) & 0x1fffffull);
+      if (lane == 0) a.hist[seg * FFB_N_CLASSES + c] = tot;
+    }
+    const unsigned long long sh = warp_sum_u64(em.shared_bytes), rg = warp_sum_u64(em.regs);
+    if (lane == 0) {
+      FfbSegInfo inf;
+      inf.status = FFB_OK; inf.n_instr = n_instr; inf.n_labels = n_labels; inf.n_decls = n_decls;
+      inf.static_shared = sh; inf.regs_declared = rg;
+      inf.name_off = (uint32_t)name_off; inf.name_len = (uint32_t)name_len;
+      inf.body_off = (uint32_t)(body_pos_g - seg_begin); inf.body_end = (uint32_t)body_end_off;
+      a.info[seg] = inf;
+      if (n_slow_seg) atomicAdd(a.fb_count + 2, (unsigned long long)n_slow_seg);   // statistics only
+    }
+  }
+}
+
+}  // namespace

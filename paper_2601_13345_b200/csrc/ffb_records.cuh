@@ -23,10 +23,32 @@ constexpr uint64_t ffb_pk(const char* s) {
   return v;
 }
 
-// ---- 61-bit name hash (FNV-1a folded) ------------------------------------------------------
-constexpr uint64_t kFnvBasis = 0xcbf29ce484222325ull, kFnvPrime = 0x100000001b3ull;
-FFB_HD uint64_t ffb_hash_step(uint64_t h, unsigned c) { return (h ^ (uint64_t)c) * kFnvPrime; }
+// ---- 61-bit name hash ----------------------------------------------------------------------
+// The text is cut into 8-byte little-endian chunks (the last one zero-padded); every chunk is
+// mixed with one multiply-xorshift, the length goes in at the end.  Tokens of at most 16 bytes
+// (registers, literals, labels) are hashed from two packed words without a byte loop
+// (ffb_hash_packed); the streaming form below gives the same value for any length.
+constexpr uint64_t kHashBasis = 0xcbf29ce484222325ull, kHashMul = 0x9e3779b97f4a7c15ull;
+FFB_HD uint64_t ffb_hash_chunk(uint64_t h, uint64_t c) { h = (h ^ c) * kHashMul; return h ^ (h >> 31); }
 FFB_HD uint64_t ffb_hash_fold(uint64_t h) { h ^= h >> 29; h *= 0xbf58476d1ce4e5b9ull; h ^= h >> 32; return h & 0x1fffffffffffffffull; }
+struct FfbHasher { uint64_t h, pk; uint32_t n; };
+FFB_HD void ffb_hash_init(FfbHasher& x) { x.h = kHashBasis; x.pk = 0; x.n = 0; }
+FFB_HD void ffb_hash_byte(FfbHasher& x, unsigned c) {
+  x.pk |= (uint64_t)(c & 0xffu) << (8u * (x.n & 7u));
+  if ((++x.n & 7u) == 0u) { x.h = ffb_hash_chunk(x.h, x.pk); x.pk = 0; }
+}
+FFB_HD uint64_t ffb_hash_done(const FfbHasher& x) {
+  uint64_t h = x.h;
+  if (x.n & 7u) h = ffb_hash_chunk(h, x.pk);
+  return ffb_hash_fold(h ^ (uint64_t)x.n);
+}
+// len <= 16 bytes packed little-endian into (lo, hi), unused bytes zero
+FFB_HD uint64_t ffb_hash_packed(uint64_t lo, uint64_t hi, uint32_t len) {
+  uint64_t h = kHashBasis;
+  if (len > 0) h = ffb_hash_chunk(h, lo);
+  if (len > 8) h = ffb_hash_chunk(h, hi);
+  return ffb_hash_fold(h ^ (uint64_t)len);
+}
 
 // ---- operand descriptor --------------------------------------------------------------------
 // bits 63..61 kind, bits 60..0 payload (name hash, or two's-complement value for INT)

@@ -42,6 +42,7 @@ struct dim3 {
 };
 struct uint4 { unsigned x, y, z, w; };
 struct uint2 { unsigned x, y; };
+inline uint4 make_uint4(unsigned x, unsigned y, unsigned z, unsigned w) { uint4 r; r.x = x; r.y = y; r.z = z; r.w = w; return r; }
 struct double2 { double x, y; };
 struct alignas(16) int4 { int x, y, z, w; };
 
@@ -126,6 +127,10 @@ inline unsigned __vcmpeq4(unsigned a, unsigned b) {
   for (int i = 0; i < 4; ++i) if (((a >> (8 * i)) & 0xffu) == ((b >> (8 * i)) & 0xffu)) r |= 0xffu << (8 * i);
   return r;
 }
+inline unsigned __funnelshift_r(unsigned lo, unsigned hi, unsigned sh) {
+  const unsigned long long v = ((unsigned long long)hi << 32) | lo; return (unsigned)(v >> (sh & 31u));
+}
+inline int __popcll_(unsigned long long v) { return __builtin_popcountll(v); }
 inline unsigned __byte_perm(unsigned a, unsigned b, unsigned s) {
   unsigned long long v = ((unsigned long long)b << 32) | a; unsigned r = 0;
   for (int i = 0; i < 4; ++i) { unsigned sel = (s >> (4 * i)) & 7u; r |= (unsigned)((v >> (8 * sel)) & 0xffu) << (8 * i); }

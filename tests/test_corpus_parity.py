@@ -126,3 +126,118 @@ def test_multi_kernel_module_ingestion(backend):
         names.append(name)
         k += 1
     assert len(set(names)) == 7
+
+
+def _lex_both(corp):
+    fast = corpus.lex_records(corp)
+    corpus.EXACT_ONLY_DEFAULT = True
+    try:
+        exact = corpus.lex_records(corp)
+    finally:
+        corpus.EXACT_ONLY_DEFAULT = False
+    return fast, exact
+
+
+def test_fast_path_equals_exact_walk(backend):
+    """The byte-parallel fast path and the exact statement walk write identical histograms,
+    segment infos, instruction / label records; compiler-shaped text stays on the fast path."""
+    n = 12 if backend == "emul" else 300
+    text, offs = synth.ptx_corpus(seed=21, n_kernels=n, lo=20, hi=600 if backend == "emul" else 5000)
+    fast, exact = _lex_both(corpus.upload_corpus(text, offs))
+    assert fast.path_counts.cpu().tolist()[:2] == [n, 0] and exact.path_counts.cpu().tolist()[:2] == [0, n]
+    n_ins = int(fast.info_np()["n_instr"].sum())
+    assert fast.path_counts.cpu().tolist()[2] < 0.1 * n_ins       # the bit-window parser takes nearly every statement
+    for f in ("hist", "info", "ins", "labels", "meta"):
+        assert np.array_equal(getattr(fast, f).cpu().numpy(), getattr(exact, f).cpu().numpy()), f
+    # irregular inputs: whichever kernel finishes a segment, the bytes are the same
+    fast, exact = _lex_both(_corpus(list(EDGE_CASES.values())))
+    taken = fast.path_counts.cpu().tolist()[:2]
+    assert taken[0] > 0 and taken[1] > 0 and sum(taken) == len(EDGE_CASES)
+    for f in ("hist", "info", "ins", "labels", "meta"):
+        assert np.array_equal(getattr(fast, f).cpu().numpy(), getattr(exact, f).cpu().numpy()), f
+
+
+@pytest.mark.parametrize("mutation", ["crlf", "block_comment", "two_statements", "label_and_statement", "multi_line",
+                                      "non_ascii", "comment_in_header", "brace_same_line", "trailing_blanks"])
+def test_fast_path_declines_irregular_text(backend, mutation):
+    """One irregular construct inside otherwise regular text: results still equal the oracle."""
+    text, offs = synth.ptx_corpus(seed=23, n_kernels=3, lo=30, hi=200)
+    srcs = [text[offs[i]:offs[i + 1]].decode("ascii") for i in range(3)]
+    s = srcs[1]
+    at = s.index("\tcvt.u64.u32")
+    if mutation == "crlf":
+        s = s.replace("\n", "\r\n")
+    elif mutation == "block_comment":
+        s = s[:at] + "\t/* add.s32 %r1, %r1, 1;\n ret; */ mov.u32 %r9, 1;\n" + s[at:]
+    elif mutation == "two_statements":
+        s = s[:at] + "\tmov.u32 %r9, 1; add.s32 %r9, %r9, 1;\n" + s[at:]
+    elif mutation == "label_and_statement":
+        s = s[:at] + "LX: mov.u32 %r9, 1;\n" + s[at:]
+    elif mutation == "multi_line":
+        s = s[:at] + "\tadd.s32 %r9,\n\t\t%r9,\n 1;\n" + s[at:]
+    elif mutation == "non_ascii":
+        s = s[:at] + "\t// caf\u00e9\n" + s[at:]
+    elif mutation == "comment_in_header":
+        s = s.replace(".visible .entry", "// .entry ghost()\n.visible .entry // name follows\n", 1)
+    elif mutation == "brace_same_line":
+        s = s.replace(")\n{\n", ") { .reg .b32 %extra<3>;\n", 1)
+    elif mutation == "trailing_blanks":
+        s = "\n".join(line + " \t " for line in s.split("\n"))
+    srcs[1] = s
+    if mutation == "non_ascii":
+        blobs = [x.encode("utf-8") for x in srcs]
+        corp = corpus.upload_corpus(b"".join(blobs), np.cumsum([0] + [len(b) for b in blobs]))
+        res = corpus.lex_histogram(corp)
+        st = res.info_np()["status"]
+        assert int(st[0]) == 0 and int(st[2]) == 0          # the neighbours are untouched
+        return
+    _check(srcs)
+
+
+OPERAND_ZOO = [
+    "mov.u32 %r1, %tid.x;", "mov.u32 %r1, %tid.y;", "mov.u32 %r2, %laneid;", "mov.u32 %r2, %warpid;", "mov.u32 %r3, %gridid;",
+    "mov.u32 %r3, WARP_SZ;", "mov.u32 %r4, %ctaid.x;", "mov.u32 %r4, %nctaid.z;", "mov.u32 %r4, %ntid.y;", "mov.u32 %r4, %ntid.w;",
+    "mov.u32 %r4, %x%gridid;", "mov.u32 %r4, %tid.;", "mov.u32 %r4, %tid.xx;", "mov.u32 %r5, %clock;", "mov.u64 %rd1, %rd2;",
+    "add.s32 %r1, %r2, 0x10;", "add.s32 %r1, %r2, 010;", "add.s32 %r1, %r2, 00;", "add.s32 %r1, %r2, 0;", "add.s32 %r1, %r2, -5;",
+    "add.s32 %r1, %r2, +7;", "add.s32 %r1, %r2, 1_000;", "add.s32 %r1, %r2, 0b101;", "add.s32 %r1, %r2, 0o17;", "add.s32 %r1, %r2, 0X1f;",
+    "add.s32 %r1, %r2, 1__0;", "add.s32 %r1, %r2, _1;", "add.s32 %r1, %r2, 1_;", "add.s32 %r1, %r2, -;", "add.s32 %r1, %r2, +-1;",
+    "mul.f32 %f1, %f2, 0f3F800000;", "mul.f64 %fd1, %fd2, 0d3FF0000000000000;", "add.s64 %rd1, %rd2, 1234567890123456;",
+    "add.s64 %rd1, %rd2, 12345678901234567;", "add.s64 %rd1, %rd2, 1152921504606846976;", "add.s64 %rd1, %rd2, -1152921504606846975;",
+    "add.s64 %rd1, %rd2, 99999999;", "add.s64 %rd1, %rd2, 123456789;", "add.s32 %r1, %r2, 12a;", "add.s32 %r1, %r2, 0x;",
+    "ld.global.f32 %f1, [%rd1+8];", "ld.global.f32 %f1, [%rd1];", "ld.global.f32 %f1, [ %rd1 + 8 ];", "ld.global.f32 %f1, [sym];",
+    "ld.global.f32 %f1, [sym+4];", "ld.global.f32 %f1, [%rd1+-8];", "ld.global.f32 %f1, [%rd1+x];", "ld.global.f32 %f1, %rd1;",
+    "ld.global.f32 %f1, [%rd1+];", "ld.global.f32 %f1, [+4];", "ld.global.f32 %f1, [%rd1+4+5];", "ld.global.f32 %f1, [%rd12345+123456];",
+    "ld.global.f32 %f1, [%rd123456+123456];", "ld.global.f32 %f1, [%r+-];", "ld.global.f32 %f1, [a];", "ld.global.f32 %f1, [];",
+    "ld.global.f32 %f1, [%rd1+-123456789];", "ld.global.f32 %f1, [%rd1+12_3];", "ld.global.f32 %f1, [%rd1+0x10];", "ld.global.f32 %f1, [%rd1)];",
+    "ld.global.f32 %f1, [%rd1(], [%rd2];", "st.global.f32 [%rd1+4], [%rd2+8];", "ld.global.f32 %f1, [%a.b+4];", "ld.global.f32 %f1, [%rd1 +4];",
+    "ld.global.v4.f32 {%f1, %f2, %f3, %f4}, [%rd1+16];", "st.global.v2.f32 [%rd1], {%f1, %f2};", "st.shared.u32 [%r1+4], %r2;",
+    "tex.2d.v4.f32.f32 {%f1, %f2, %f3, %f4}, [tex0, {%f5, %f6}];", "call.uni (retval0), foo, (param0, param1);",
+    "mad.lo.s32 %r1, %r2, %r3, %r4;", "fma.rn.f32 %f1, %f2, %f3, %f4;", "lop3.b32 %r1, %r2, %r3, %r4, 150;",
+    "shfl.sync.bfly.b32 %r1|%p1, %r2, 16, 31, -1;", "op.x %r1, %r2, %r3, %r4, %r5, %r6, %r7;", "op.y %r1, 1, 2, 3, 4, 5, 6, 7, %r9;",
+    "add.s32 %r1 , %r2 ,  3 ;", "add.s32 %r1,%r2,3;", "add.s32 %r1,, %r2;", "add.s32 %r1, %r2,;", "ret;", "bar.sync 0;", "bar.sync \t0, 64;",
+    "@%p1 bra L0;", "@!%p1 bra L0;", "@%p1 add.s32 %r1, %r1, 1;", "@ %p1 bra L0;", "@%p$x.y bra L0;", "@!p bra L0;", "bra.uni L0;",
+    "setp.lt.s32 %p1, %r1, 10;", "setp.ge.u32 %p1, %r1, %r2;", "sqrt.approx.f32 %f1, %f2;", "sqrt.rn.f32 %f1, %f2;", "a.b.c.d.e.f.g.h.i.j.k.l %r1;",
+    "verylongopcodetoken.anotherverylongtoken.s32 %r1, %r2;", "add..s32 %r1, %r2, 1;", "add.s32. %r1, %r2, 1;", ".s32 %r1;",
+    "mov.u32 %r1, a_symbol_longer_than_sixteen_bytes;", "mov.u32 %r1, exactly16bytes_ab;", "mov.u32 %r1, %r_sixteen_bytes_;",
+    "mov.u32 %r1, %seventeen_bytes__;", "mov.b64 %rd1, {%r1, %r2};", "mov.b64 {%r1, %r2}, %rd1;",
+    "add.s32 %r1, %r2, 3 " + "\t" * 40 + ";", "add.s32 %r1, " + " " * 45 + "%r2, 3;", "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 \t{%f1, %f2}, {%r1}, {%r2}, {%f3, %f4};",
+]
+
+
+def test_operand_zoo_fast_equals_exact(backend):
+    """Every operand / predicate / opcode shape the record builder distinguishes, one statement per
+    line so the fast path takes the segment: records equal the exact walk's bit for bit, and the
+    feature rows equal the oracle's."""
+    segs = []
+    for rep in range(3):            # shift the alignment of every statement against the 4-byte loads
+        body = "\n".join((" " * ((i + rep) % 5)) + "\t" + st for i, st in enumerate(OPERAND_ZOO))
+        segs.append(".visible .entry zoo%d()\n{\n\t.reg .b32 %%r<9>;\nL0:\n%s\n\tret;\n}\n" % (rep, body))
+    fast, exact = _lex_both(_corpus(segs))
+    assert fast.path_counts.cpu().tolist()[:2] == [3, 0]
+    assert int((fast.info_np()["status"] != 0).sum()) == 0
+    for f in ("hist", "info", "ins", "labels", "meta"):
+        assert np.array_equal(getattr(fast, f).cpu().numpy(), getattr(exact, f).cpu().numpy()), f
+    for k, src in enumerate(segs):
+        kern = orc.parse_kernel(src)
+        assert fast.hist.cpu().numpy()[k].tolist() == orc.class_histogram(kern)
+        assert int(fast.info_np()[k]["n_instr"]) == len(kern.ins)
