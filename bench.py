@@ -43,6 +43,7 @@ def parse_args():
     ap.add_argument("--kernels", type=int, default=KERNELS_PER_RANK, help="kernels per rank")
     ap.add_argument("--corpus-mb", type=int, default=-1, help="PTX shard per rank in MB (-1: 1250 when the lexer is built)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lex-flags", type=int, default=0, help="FFB_LEX_* bits for A/B runs (2 = no lock-step CTAs)")
     return ap.parse_args()
 
 
@@ -172,6 +173,8 @@ def main():
 
     corpus = None
     corpus_mb = args.corpus_mb if args.corpus_mb >= 0 else (1250 if corpus_mod is not None else 0)
+    if corpus_mod is not None:
+        corpus_mod.LEX_FLAGS_DEFAULT = args.lex_flags
     if corpus_mod is not None and corpus_mb > 0:
         corpus = corpus_mod.bench_corpus(seed=4 + rank, target_bytes=corpus_mb * 10**6, n_kernels=K)
 

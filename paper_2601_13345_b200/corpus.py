@@ -103,6 +103,8 @@ class LexResult:
 
 
 LEX_EXACT_ONLY = 1
+LEX_NO_LOCKSTEP = 2
+LEX_FLAGS_DEFAULT = 0          # extra FFB_LEX_* bits for every call (benchmark A/B switches)
 EXACT_ONLY_DEFAULT = False      # tests flip this to run the exact statement walk alone
 
 
@@ -116,7 +118,7 @@ def _call_lex(rt, corp: Corpus, hist, info, *, kernel_name: bytes | None = None,
         d_hist=native.ptr(hist), d_info=native.ptr(info), d_ins_base=native.ptr(ins_base),
         d_lab_base=native.ptr(lab_base), d_ins_cap=native.ptr(ins_cap), d_lab_cap=native.ptr(lab_cap), d_ins=native.ptr(ins), d_labels=native.ptr(labels),
         d_meta=native.ptr(meta), d_spans=native.ptr(spans), d_decls=native.ptr(decls),
-        flags=LEX_EXACT_ONLY if (exact_only or EXACT_ONLY_DEFAULT) else 0, d_path_counts=native.ptr(path_counts))
+        flags=(LEX_EXACT_ONLY if (exact_only or EXACT_ONLY_DEFAULT) else 0) | LEX_FLAGS_DEFAULT, d_path_counts=native.ptr(path_counts))
     rc = rt.lib.ffb_lex_corpus(rt.ctx, C.byref(d), rt.stream())
     rt.check(rc, "ffb_lex_corpus")
 

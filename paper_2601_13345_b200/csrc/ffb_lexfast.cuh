@@ -152,8 +152,17 @@ FFB_D uint64_t packed_tail(uint64_t lo, uint64_t hi, int len, int k) {
   const uint64_t v = sh == 0 ? lo : (sh >= 64 ? hi >> (sh - 64) : (lo >> sh) | (hi << (64 - sh)));
   return v & low_mask(8 * k);
 }
-FFB_D uint64_t hash_span(const uint8_t* s, int a, int b) {      // norm_hash of a span without newlines
-  if (b - a > 16 || b <= a) return cold_norm_hash(s, a, b);
+// name hash of s[a,b) when the span holds no newline (every statement of the fast path sits on one
+// line, so norm_hash's blank-run rule never fires): 8-byte chunks straight from packed loads
+FFB_D uint64_t hash_bytes(const uint8_t* s, int a, int len) {
+  uint64_t h = kHashBasis;
+#pragma unroll 1
+  for (int off = 0; off < len; off += 8) h = ffb_hash_chunk(h, load_packed(s, a + off, len - off < 8 ? len - off : 8));
+  return ffb_hash_fold(h ^ (uint64_t)(uint32_t)len);
+}
+FFB_D uint64_t hash_span(const uint8_t* s, int a, int b) {
+  if (b <= a) return cold_norm_hash(s, a, b);
+  if (b - a > 16) return hash_bytes(s, a, b - a);
   uint64_t lo, hi;
   load_packed16(s, a, b - a, &lo, &hi);
   return ffb_hash_packed(lo, hi, (uint32_t)(b - a));
@@ -164,7 +173,12 @@ FFB_D uint64_t hash_span(const uint8_t* s, int a, int b) {      // norm_hash of 
 // grammar (prefixed or '_'-separated literals) and longer operands use describe_operand itself.
 FFB_D uint64_t describe_fast(const uint8_t* s, int a, int b) {
   const int len = b - a;
-  if (len > 16) return cold_describe_operand(s, a, b);
+  if (len > 16) {
+    // long operands are vector lists and symbols; registers and numbers this long take the byte walk
+    const unsigned f = s[a];
+    if (f == '%' || f == '+' || f == '-' || ffb_is_digit(f)) return cold_describe_operand(s, a, b);
+    return ffb_op_make(FFB_OPK_UNIFORM, hash_bytes(s, a, len));
+  }
   uint64_t lo, hi;
   load_packed16(s, a, len, &lo, &hi);
   const uint64_t h = ffb_hash_packed(lo, hi, (uint32_t)len);
@@ -262,7 +276,6 @@ FFB_D bool address_fast(const uint8_t* s, int a, int b, uint32_t* kind, uint64_t
 template <int kMode>
 FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, int kb, int ke, Emit& em) {
   const int n = ke - kb;
-  if (kMode == 2 && n > 64) return false;
   const int w0 = kb >> 5, sh = kb & 31;
   const uint64_t valid = low_mask(n);
   uint64_t BL, DT;
@@ -323,21 +336,27 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
   const OpcodeInfo oc = finish_opcode(base, elem_code, vec, space, cmp, flags);
   if (kMode == 2) {
     // ---- operands: top-level commas (ptx.py:144-162) ----
-    uint64_t CM, OP, CL;
+    // a second set of windows, anchored at the end of the opcode, so that the operand list may
+    // itself be 64 bytes long (mma / tex / vector forms with a long opcode in front)
+    const int ko = kb + o1, m = n - o1;
+    if (m > 64) return false;
+    uint64_t BO, CM, OP, CL;
     {
-      const uint4 b0 = MB[w0], b1 = MB[w0 + 1], b2 = MB[w0 + 2];
-      CM = win64(b0.x, b1.x, b2.x, sh); OP = win64(b0.y, b1.y, b2.y, sh); CL = win64(b0.z, b1.z, b2.z, sh);
+      const int wo = ko >> 5, so = ko & 31;
+      const uint64_t R = low_mask(m);
+      const uint4 a0 = MA[wo], a1 = MA[wo + 1], a2 = MA[wo + 2];
+      const uint4 b0 = MB[wo], b1 = MB[wo + 1], b2 = MB[wo + 2];
+      BO = win64(a0.z, a1.z, a2.z, so) & R;
+      CM = win64(b0.x, b1.x, b2.x, so) & R; OP = win64(b0.y, b1.y, b2.y, so) & R; CL = win64(b0.z, b1.z, b2.z, so) & R;
     }
-    const uint64_t R = valid & high_mask(o1);
-    const uint64_t NB = ~BL & R;
-    OP &= R; CL &= R;
+    const uint64_t NB = ~BO & low_mask(m);
     uint64_t inside = 0;
     if (OP | CL) {                                    // brackets must alternate open / close (depth 0 or 1)
       const uint64_t X = OP | CL, incl = prefix_xor64(X), excl = incl ^ X;
       if ((OP & excl) || (CL & ~excl) || (__popcll(X) & 1)) return false;
       inside = incl;
     }
-    const uint64_t C0 = CM & R & ~inside;
+    const uint64_t C0 = CM & ~inside;
     const bool is_mem = oc.cls == FFB_CLS_MEMLOAD || oc.cls == FFB_CLS_MEMSTORE;
     const bool aux_is_op4 = !is_mem && oc.cls != FFB_CLS_BRANCH;
     FfbInsRec rec;
@@ -346,15 +365,15 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
     bool extra_reg = false, dst_reg = false;
     {
       uint64_t rem = C0;
-      int from = o1;
+      int from = 0;
       for (;;) {
-        const int to = rem ? __ffsll((long long)rem) - 1 : n;
+        const int to = rem ? __ffsll((long long)rem) - 1 : m;
         const uint64_t seg = NB & low_mask(to) & high_mask(from);
         if (!seg) {
           if (C0) return false;                       // empty operand between commas: the walk drops it
           break;
         }
-        const int a = kb + __ffsll((long long)seg) - 1, b = kb + 64 - __clzll((long long)seg);
+        const int a = ko + __ffsll((long long)seg) - 1, b = ko + 64 - __clzll((long long)seg);
         const unsigned c_first = s[a];
         if (count == 0) dst_reg = c_first == '%';
         if (count < 4 || (count == 4 && aux_is_op4)) {
@@ -373,8 +392,8 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
     uint32_t addr_kind = FFB_ADDR_ABSENT;
     if (is_mem) {
       if (as >= 0) {
-        const uint64_t span = low_mask(ae - kb) & high_mask(as - kb);
-        const bool canonical = ae - as <= 16 && !(BL & span) && ((OP | CL) & span) == ((1ull << (as - kb)) | (1ull << (ae - kb - 1)));
+        const uint64_t span = low_mask(ae - ko) & high_mask(as - ko);
+        const bool canonical = ae - as <= 16 && !(BO & span) && ((OP | CL) & span) == ((1ull << (as - ko)) | (1ull << (ae - ko - 1)));
         if (!canonical || !address_fast(s, as, ae, &addr_kind, &rec.aux)) {
           const AddrDesc ad = cold_describe_address(s, as, ae);
           addr_kind = ad.kind; rec.aux = ad.desc;
@@ -384,7 +403,7 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
     else if (!aux_is_op4) rec.aux = last_s >= 0 ? ffb_op_make(FFB_OPK_REG, hash_span(s, last_s, last_e)) : 0ull;
     rec.line = em.line;
     rec.off = (uint32_t)(em.abase + kb - em.seg_begin);
-    rec.len = (uint32_t)(64 - __clzll((long long)(~BL & valid)));
+    rec.len = (uint32_t)(NB ? o1 + 64 - __clzll((long long)NB) : o1);
     rec.pred = has_pred ? hash_span(s, p0, p1) : 0ull;
     rec.meta = oc.cls | (oc.space << 4) | ((oc.bytes & 63u) << 7) | (oc.base << 13) | ((has_pred ? 1u : 0u) << 18) |
                ((neg ? 1u : 0u) << 19) | ((uint32_t)(count > 7 ? 7 : count) << 20) | (oc.cmp << 23) | (addr_kind << 26) |
@@ -495,8 +514,12 @@ FFB_D bool in_line_comment(const uint8_t* s, int at, int lo) {   // is a "//" op
   return false;
 }
 
-template <bool kRecords>
-__global__ void __launch_bounds__(kFWarps * 32, kRecords ? 4 : 6)
+// kLockstep: one CTA fills the SM and its warps meet at a barrier before every tile, so that the
+// warps of a scheduler run the same phase of the (long) tile loop together and share fetched
+// instruction lines; without it 70% of the issue slots of the record-mode kernel waited for
+// instruction fetch (ncu r1o).
+template <bool kRecords, bool kLockstep>
+__global__ void __launch_bounds__(kLockstep ? (kRecords ? 512 : 768) : kFWarps * 32, kLockstep ? 1 : (kRecords ? 4 : 6))
 lex_fast_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
@@ -513,9 +536,9 @@ lex_fast_kernel(LexArgs a) {
   uint32_t* P = reinterpret_cast<uint32_t*>(s + kFOffP);
   uint16_t* nl = reinterpret_cast<uint16_t*>(s + kFOffNl);
   uint32_t* linfo = reinterpret_cast<uint32_t*>(s + kFOffInfo);
-  for (int c = threadIdx.x; c < 256; c += kFWarps * 32) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
+  for (int c = threadIdx.x; c < 256; c += (int)blockDim.x) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
   __syncthreads();
-  for (int c = threadIdx.x; c < kNumTokDefs; c += kFWarps * 32) {
+  for (int c = threadIdx.x; c < kNumTokDefs; c += (int)blockDim.x) {
     const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
     s_tok_key[slot] = kTokDefs[c].key; s_tok_val[slot] = kTokDefs[c].val;
   }
@@ -526,33 +549,44 @@ lex_fast_kernel(LexArgs a) {
   }
   __syncthreads();
 
+  // one segment in flight per warp; the loop below handles ONE tile per trip
+  bool have = false, done = false, reject = false;
+  int64_t seg = 0, seg_begin = 0, seg_end = 0, cur = 0, scan_from_g = 0, body_pos_g = 0;
+  int64_t name_off = 0, name_len = 0, body_end_off = 0, ins_base = 0, lab_base = 0;
+  int phase = PH_SEARCH, depth = 0;
+  uint32_t line_no = 1, n_instr = 0, n_labels = 0, n_decls = 0, n_slow_seg = 0;
+  Emit em;
+  em.a = &a; em.abase = 0; em.line = 0; em.dcl_at = 0;
+  em.tok.key = s_tok_key; em.tok.val = s_tok_val; em.cls = s_cls;
+  em.seg = 0; em.seg_begin = 0; em.ins_at = 0; em.lab_at = 0; em.ins_limit = 0; em.lab_limit = 0;
+  em.c0 = em.c1 = em.c2 = 0; em.shared_bytes = 0; em.regs = 0;
+
   for (;;) {
-    unsigned long long wq = 0;
-    if (lane == 0) wq = atomicAdd(a.work, 1ull);
-    wq = __shfl_sync(kFull, wq, 0);
-    if (wq >= (unsigned long long)a.n_segs) break;
-    const int64_t seg = a.order ? (int64_t)a.order[wq] : (int64_t)wq;
-    const int64_t seg_begin = a.seg_off[seg], seg_end = a.seg_off[seg + 1];
+    if (!have && !done) {
+      unsigned long long wq = 0;
+      if (lane == 0) wq = atomicAdd(a.work, 1ull);
+      wq = __shfl_sync(kFull, wq, 0);
+      if (wq >= (unsigned long long)a.n_segs) done = true;
+      else {
+        have = true;
+        seg = a.order ? (int64_t)a.order[wq] : (int64_t)wq;
+        seg_begin = a.seg_off[seg]; seg_end = a.seg_off[seg + 1];
+        phase = PH_SEARCH; depth = 0; reject = false; line_no = 1;
+        cur = seg_begin; scan_from_g = seg_begin; body_pos_g = 0;
+        name_off = 0; name_len = 0; body_end_off = 0;
+        n_instr = 0; n_labels = 0; n_decls = 0; n_slow_seg = 0;
+        ins_base = kRecords ? a.ins_base[seg] : 0; lab_base = kRecords ? a.lab_base[seg] : 0;
+        em.seg = seg; em.seg_begin = seg_begin; em.ins_at = ins_base; em.lab_at = lab_base;
+        em.ins_limit = (kRecords && a.ins_cap) ? ins_base + a.ins_cap[seg] : 0x7fffffffffffffffLL;
+        em.lab_limit = (kRecords && a.lab_cap) ? lab_base + a.lab_cap[seg] : 0x7fffffffffffffffLL;
+        em.c0 = em.c1 = em.c2 = 0; em.shared_bytes = 0; em.regs = 0;
+      }
+    }
+    if (kLockstep) { if (!__syncthreads_or(done ? 0 : 1)) break; }
+    else if (done) break;
+    if (done) continue;                                          // idle warps keep meeting the barrier
 
-    int phase = PH_SEARCH, depth = 0;
-    bool reject = false;
-    uint32_t line_no = 1;
-    int64_t cur = seg_begin, scan_from_g = seg_begin, body_pos_g = 0;
-    int64_t name_off = 0, name_len = 0, body_end_off = 0;
-    uint32_t n_instr = 0, n_labels = 0, n_decls = 0, n_slow_seg = 0;
-    const int64_t ins_base = kRecords ? a.ins_base[seg] : 0, lab_base = kRecords ? a.lab_base[seg] : 0;
-
-    Emit em;
-    em.a = &a; em.seg = seg; em.seg_begin = seg_begin; em.abase = 0; em.line = 0;
-    em.tok.key = s_tok_key; em.tok.val = s_tok_val; em.cls = s_cls;
-    em.ins_at = ins_base; em.lab_at = lab_base;
-    em.ins_limit = (kRecords && a.ins_cap) ? ins_base + a.ins_cap[seg] : 0x7fffffffffffffffLL;
-    em.lab_limit = (kRecords && a.lab_cap) ? lab_base + a.lab_cap[seg] : 0x7fffffffffffffffLL;
-    em.dcl_at = 0;
-    em.c0 = em.c1 = em.c2 = 0;
-    em.shared_bytes = 0; em.regs = 0;
-
-    while (phase != PH_DONE && cur < seg_end) {
+    if (cur < seg_end) do {
       const int64_t abase = cur & ~(int64_t)15;
       const int64_t hi_g = (abase + kFTile < seg_end) ? abase + kFTile : seg_end;
       const int lo = (int)(cur - abase), hi = (int)(hi_g - abase);
@@ -831,12 +865,14 @@ lex_fast_kernel(LexArgs a) {
       const int64_t next = abase + region_end;
       if (next <= cur) { reject = true; break; }
       cur = next;
-    }
+    } while (0);
+    if (!(phase == PH_DONE || reject || cur >= seg_end)) continue;   // more tiles of this segment
 
     // ================= segment epilogue =================
     // only complete, well-formed kernels are finished here; every error status comes from the exact kernel
-    bool ok = !reject && phase == PH_DONE && n_instr > 0;
+    bool ok = !reject && phase == PH_DONE && n_instr > 0;   // (an empty segment ends here too: nothing found)
     if (kRecords && ok && ((a.ins_cap && (int64_t)n_instr > a.ins_cap[seg]) || (a.lab_cap && (int64_t)n_labels > a.lab_cap[seg]))) ok = false;
+    have = false;
     if (!ok) {
       if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1ull)] = (int32_t)seg;
       continue;

@@ -55,6 +55,7 @@ struct Cta {
   pthread_barrier_t bar;
   std::vector<WarpBox*> warps;
   unsigned nthreads;
+  int vote = 0;
 };
 extern thread_local uint3_ t_threadIdx, t_blockIdx;
 extern thread_local dim3 t_blockDim, t_gridDim;
@@ -71,6 +72,16 @@ void launch(dim3 grid, dim3 block, size_t smem, const std::function<void()>& bod
 static const int warpSize = 32;
 
 inline void __syncthreads() { pthread_barrier_wait(&simt::t_cta->bar); }
+inline int __syncthreads_or(int p) {
+  simt::Cta* c = simt::t_cta;
+  if (p) __atomic_store_n(&c->vote, 1, __ATOMIC_SEQ_CST);
+  pthread_barrier_wait(&c->bar);
+  const int r = __atomic_load_n(&c->vote, __ATOMIC_SEQ_CST);
+  pthread_barrier_wait(&c->bar);
+  if (threadIdx.x == 0) __atomic_store_n(&c->vote, 0, __ATOMIC_SEQ_CST);
+  pthread_barrier_wait(&c->bar);
+  return r;
+}
 inline void __syncwarp(unsigned = 0xffffffffu) { pthread_barrier_wait(&simt::t_warp->bar); }
 inline void __threadfence() { std::atomic_thread_fence(std::memory_order_seq_cst); }
 inline void __threadfence_block() { std::atomic_thread_fence(std::memory_order_seq_cst); }
