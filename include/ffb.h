@@ -291,7 +291,9 @@ typedef struct {
   uint8_t* d_loop_body;           /* single-segment use: n_loops x n_blocks membership matrix   */
   int64_t loop_body_cap;          /* bytes available behind d_loop_body                         */
   double* d_weights;              /* [n_ins_total + 2K + 8] block weights (cfg.py:43-54)        */
+  uint32_t flags;                 /* FFB_FLOW_* bits                                            */
 } FfbFlowDesc;
+#define FFB_FLOW_SEQUENTIAL_PASS 1u   /* textual pass on one lane only (the general form; default: 32 statements per round) */
 int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, void* stream);
 /* 61-bit name hash the lexer assigns to labels / registers (for annotation keys). */
 uint64_t ffb_name_hash(const uint8_t* name, int64_t len);

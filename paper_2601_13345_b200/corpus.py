@@ -104,6 +104,8 @@ class LexResult:
 
 LEX_EXACT_ONLY = 1
 LEX_NO_LOCKSTEP = 2
+FLOW_SEQUENTIAL_PASS = 1
+FLOW_FLAGS_DEFAULT = 0         # FFB_FLOW_* bits for every call (tests flip this)
 LEX_FLAGS_DEFAULT = 0          # extra FFB_LEX_* bits for every call (benchmark A/B switches)
 EXACT_ONLY_DEFAULT = False      # tests flip this to run the exact statement walk alone
 
@@ -209,6 +211,7 @@ class FlowDesc(C.Structure):
         ("h_ann_trip", C.c_void_p), ("n_ann", C.c_int32), ("d_ann_hit", C.c_void_p), ("d_feat", C.c_void_p),
         ("d_status", C.c_void_p), ("d_flow", C.c_void_p), ("d_block_start", C.c_void_p), ("d_edges", C.c_void_p),
         ("d_loops", C.c_void_p), ("d_loop_body", C.c_void_p), ("loop_body_cap", C.c_int64), ("d_weights", C.c_void_p),
+        ("flags", C.c_uint32),
     ]
 
 
@@ -267,7 +270,8 @@ def kernel_features(corp: Corpus, lex: LexResult, *, default_trip: float = 32.0,
         n_ann=n_ann, d_ann_hit=native.ptr(res.ann_hit), d_feat=native.ptr(feat), d_status=native.ptr(status),
         d_flow=native.ptr(res.flow), d_block_start=native.ptr(res.block_start), d_edges=native.ptr(res.edges),
         d_loops=native.ptr(res.loops), d_loop_body=native.ptr(res.loop_body),
-        loop_body_cap=int(res.loop_body.numel()) if res.loop_body is not None else 0, d_weights=native.ptr(res.weights))
+        loop_body_cap=int(res.loop_body.numel()) if res.loop_body is not None else 0, d_weights=native.ptr(res.weights),
+        flags=FLOW_FLAGS_DEFAULT)
     rc = rt.lib.ffb_kernel_features(rt.ctx, C.byref(d), rt.stream())
     rt.check(rc, "ffb_kernel_features")
     return res

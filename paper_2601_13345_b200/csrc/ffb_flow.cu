@@ -31,7 +31,8 @@
 namespace {
 
 constexpr int kFlowWarps = 4;
-constexpr int kCacheSlots = 256;
+constexpr int kMapSlots = 512;                    // shared-memory register -> scale map per warp (8 KB)
+constexpr int kMapFill = 384;                     // entries kept on chip; later names spill to the HBM table
 constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
 constexpr uint32_t kNoBlock = 0xffffffffu;
@@ -47,6 +48,7 @@ struct FlowArgs {
   const int32_t* order;
   unsigned long long* work;     // work-queue counter
   double default_trip;
+  int parallel_pass;            // 0: textual pass on lane 0 only (test switch)
   const uint64_t* ann_hash;     // device copies
   const double* ann_trip;
   int n_ann;
@@ -201,21 +203,35 @@ FFB_D int warp_sum_i(int v) {
   return v;
 }
 
-// Write-through cache of the register -> scale table in shared memory (direct mapped).  Most
-// sources were defined a few statements earlier, so most look-ups never leave the SM.
+// Register -> scale map of the textual pass (alignment.py:61-125).  The first kMapFill distinct
+// names live in an open-addressing table in shared memory, so the sequential walk never leaves
+// the SM for ordinary kernels (r1i: 80% of the stall samples of this kernel were lane 0 waiting
+// on the HBM-resident table).  Names met after that go to the HBM table `g`, cleared lazily on
+// the first spill.  Used by lane 0 only.
 struct CachedScales {
   ScaleTable g;
   uint64_t* ckey; int64_t* cval;
+  uint32_t used; bool spilled;
   FFB_D int64_t get(uint64_t h) {
-    const uint32_t c = (uint32_t)(h ^ (h >> 17)) & (kCacheSlots - 1);
-    if (ckey[c] == h + 1) return cval[c];
-    const int64_t v = g.get(h);
-    ckey[c] = h + 1; cval[c] = v;
-    return v;
+    uint32_t c = slot_of(h, kMapSlots);
+    for (;;) {
+      const uint64_t k = ckey[c];
+      if (k == h + 1) return cval[c];
+      if (k == 0) break;
+      c = (c + 1) & (kMapSlots - 1);
+    }
+    return spilled ? g.get(h) : kNoneScale;
   }
   FFB_D void put(uint64_t h, int64_t v) {
-    const uint32_t c = (uint32_t)(h ^ (h >> 17)) & (kCacheSlots - 1);
-    ckey[c] = h + 1; cval[c] = v;
+    uint32_t c = slot_of(h, kMapSlots);
+    for (;;) {
+      const uint64_t k = ckey[c];
+      if (k == h + 1) { cval[c] = v; return; }
+      if (k == 0) break;
+      c = (c + 1) & (kMapSlots - 1);
+    }
+    if (used < kMapFill) { ckey[c] = h + 1; cval[c] = v; ++used; return; }
+    if (!spilled) { g.clear(); spilled = true; }
     g.put(h, v);
   }
 };
@@ -236,6 +252,80 @@ FFB_D int64_t mul_scale_c(uint64_t a, uint64_t b, CachedScales& t) {
   return kNoneScale;
 }
 
+// ---- one statement of the textual pass, from the scales of its sources ------------------------------
+// s1..s3 / sa: scales of operands 1..3 and of the `aux` descriptor (alignment.py:31-47), however the
+// caller obtained them (table look-up, or the value an earlier statement of the same chunk published).
+struct SrcScales { int64_t s1, s2, s3, sa; };
+FFB_D int64_t mul_scale_v(uint64_t a, uint64_t b, int64_t sa, int64_t sb) {          // alignment.py:50-58
+  if (sa == 0 && sb == 0) return 0;
+  if (is_int_lit(b) && sc_known(sa)) return sc_mul(sa, int_as_scale(b));
+  if (is_int_lit(a) && sc_known(sb)) return sc_mul(int_as_scale(a), sb);
+  return kNoneScale;
+}
+// Non-memory statement with a register destination (alignment.py:91-125): the scale it defines.
+// Returns false for setp (no definition).
+FFB_D bool eval_def(uint32_t m, uint64_t op1, uint64_t op2, uint64_t op3, const SrcScales& s, int64_t* out, uint32_t* status) {
+  const uint32_t nops = ffb_meta_nops(m), base = ffb_meta_base(m);
+  int64_t v;
+  if (base == FFB_BASE_MOV && nops == 2) v = s.s1;
+  else if ((base == FFB_BASE_CVT || base == FFB_BASE_CVTA) && nops >= 2) {
+    v = nops == 2 ? s.s1 : nops == 3 ? s.s2 : nops == 4 ? s.s3 : s.sa;            // LAST operand
+    if (nops > 5) { *status = FFB_E_CAPACITY; v = kNoneScale; }
+  } else if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && nops == 3) {
+    v = base == FFB_BASE_ADD ? sc_add(s.s1, s.s2) : sc_add(s.s1, sc_neg(s.s2));
+  } else if (base == FFB_BASE_MUL && nops == 3) v = mul_scale_v(op1, op2, s.s1, s.s2);
+  else if ((base == FFB_BASE_MAD || base == FFB_BASE_FMA) && nops == 4) v = sc_add(mul_scale_v(op1, op2, s.s1, s.s2), s.s3);
+  else if (base == FFB_BASE_SHL && nops == 3) {
+    if (!sc_known(s.s1) || !is_int_lit(op2)) v = kNoneScale;
+    else {
+      const int64_t sh = int_as_scale(op2);
+      if (sh == kBigScale || sh < 0) { *status = FFB_E_CAPACITY; v = kNoneScale; }   // 1 << huge / negative: reference raises
+      else v = s.s1 == 0 ? 0 : (sh >= 61 ? kBigScale : sc_mul(s.s1, (int64_t)1 << sh));
+    }
+  } else if (base == FFB_BASE_SETP) return false;
+  else {
+    // unmodelled producer: uniform only if it has sources and all of them are uniform
+    bool all0 = nops >= 2;
+    if (nops > 1) all0 = all0 && s.s1 == 0;
+    if (nops > 2) all0 = all0 && s.s2 == 0;
+    if (nops > 3) all0 = all0 && s.s3 == 0;
+    if (nops >= 5) all0 = all0 && s.sa == 0;
+    if (all0 && nops >= 6 && ffb_meta_extra_reg(m)) { *status = FFB_E_CAPACITY; all0 = false; }
+    v = all0 ? 0 : kNoneScale;
+  }
+  *out = v;
+  return true;
+}
+// Per-statement contributions to the dynamic counts (features.py:62-81) and the alignment sums
+// (alignment.py:137-144); `sc_addr` is the scale of the address register of a global access.
+struct Sums { double n_mem, mem_bytes, u_fp, u_int, u_sfu, u_alu, n_sync, al_hit, al_tot; };
+FFB_D void count_statement(uint32_t m, double wgt, int64_t sc_addr, Sums& a) {
+  const uint32_t cls = ffb_meta_cls(m);
+  if (cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE) {
+    const uint32_t space = ffb_meta_space(m), bytes = ffb_meta_bytes(m);
+    if (space != FFB_SP_PARAM) { a.n_mem += wgt; a.mem_bytes += wgt * (double)bytes; }
+    if (space == FFB_SP_GLOBAL) {
+      int64_t sc = kNoneScale;
+      const uint32_t ak = ffb_meta_addr(m);
+      if (ak == FFB_ADDR_SYMBOL) sc = 0;
+      else if (ak == FFB_ADDR_REG) sc = sc_addr;
+      a.al_tot += wgt;
+      if (sc_known(sc) && sc != kBigScale && (sc < 0 ? -sc : sc) == (int64_t)bytes) a.al_hit += wgt;
+    }
+    return;
+  }
+  if (cls == FFB_CLS_FP32) a.u_fp += wgt;
+  else if (cls == FFB_CLS_INT) a.u_int += wgt;
+  else if (cls == FFB_CLS_SFU) a.u_sfu += wgt;
+  else if (cls == FFB_CLS_ALU) a.u_alu += wgt;
+  else if (cls == FFB_CLS_SYNC) a.n_sync += wgt;
+}
+FFB_D double warp_sum_d(double v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kAll, v, d);
+  return v;
+}
+
 // One WARP per kernel.  Lane-parallel: label table, leaders, block numbering, edges, the
 // "last match" scans of the trip recogniser, weights, record staging.  Lane 0 alone: the graph
 // walks (DFS, dominators, loop bodies) and the textual dataflow pass, which are sequential by
@@ -244,8 +334,11 @@ __global__ void __launch_bounds__(kFlowWarps * 32)
 flow_kernel(FlowArgs a) {
   __shared__ FfbInsRec s_stage[kFlowWarps][32];      // FfbInsRec is 16-byte aligned by declaration
   __shared__ double s_wstage[kFlowWarps][32];
-  __shared__ uint64_t s_ckey[kFlowWarps][kCacheSlots];
-  __shared__ int64_t s_cval[kFlowWarps][kCacheSlots];
+  __shared__ uint64_t s_ckey[kFlowWarps][kMapSlots];
+  __shared__ int64_t s_cval[kFlowWarps][kMapSlots];
+  __shared__ uint64_t s_chkey[kFlowWarps][64];      // chunk-local: names the 32 statements in flight define
+  __shared__ uint32_t s_chmask[kFlowWarps][64];     //              ... and the lanes that define them
+  __shared__ int64_t s_chval[kFlowWarps][32];       //              ... and the values they publish
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   FfbInsRec* stage = s_stage[wid];
   double* wstage = s_wstage[wid];
@@ -291,12 +384,11 @@ flow_kernel(FlowArgs a) {
     CachedScales st;
     st.g.key = a.sc_key + 4 * ib + 8 * k; st.g.val = a.sc_val + 4 * ib + 8 * k;
     st.g.cap = 4; while (st.g.cap < 2 * n + 2) st.g.cap <<= 1;      // <= 4n + 8
-    st.ckey = s_ckey[wid]; st.cval = s_cval[wid];
+    st.ckey = s_ckey[wid]; st.cval = s_cval[wid]; st.used = 0; st.spilled = false;
 
     // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
     for (uint32_t i = lane; i < lt.cap; i += 32) { lt.key[i] = 0; lt.first[i] = 0xffffffffu; lt.last[i] = 0; }
-    for (uint32_t i = lane; i < st.g.cap; i += 32) st.g.key[i] = 0;
-    for (uint32_t i = lane; i < kCacheSlots; i += 32) st.ckey[i] = 0;
+    for (uint32_t i = lane; i < kMapSlots; i += 32) st.ckey[i] = 0;
     for (uint32_t i = lane; i < n; i += 32) block_of[i] = 0;
     __syncwarp();
     for (uint32_t i = lane; i < L; i += 32) {
@@ -619,9 +711,146 @@ flow_kernel(FlowArgs a) {
     }
     __syncwarp();
     // ---- one textual pass: affine scales, aligned fraction, dynamic counts ----
-    double n_mem = 0.0, mem_bytes = 0.0, u_fp = 0.0, u_int = 0.0, u_sfu = 0.0, u_alu = 0.0, n_sync = 0.0;
-    double al_hit = 0.0, al_tot = 0.0;
-    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+    // Parallel form: 32 statements per round, one per lane.  A chunk-local table maps every register
+    // the chunk defines to the mask of defining lanes, so a source is either "before the chunk" (looked
+    // up in the shared-memory map, all lanes at once) or "lane j of this chunk" (read after j has
+    // published); dependent statements resolve in waves.  The last definer of each name updates the
+    // map.  The sums are accumulated per lane and reduced at the end, which is bit-identical to the
+    // reference's in-order sums whenever every partial sum is exactly representable (all weights on
+    // a 1/64 grid and the totals below 2^44 - checked here); otherwise, or when the kernel names more
+    // registers than the on-chip map holds, the pass continues sequentially on lane 0.
+    Sums acc;
+    acc.n_mem = acc.mem_bytes = acc.u_fp = acc.u_int = acc.u_sfu = acc.u_alu = acc.n_sync = acc.al_hit = acc.al_tot = 0.0;
+    bool exact_sums = true;
+    {
+      double wmax = 0.0;
+      for (uint32_t b = lane; b < nb; b += 32) {
+        const double w = weight[b], w64 = w * 64.0;
+        if (!(w64 == floor(w64))) exact_sums = false;
+        wmax = w > wmax ? w : wmax;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) { const double o = __shfl_xor_sync(kAll, wmax, d); wmax = o > wmax ? o : wmax; }
+      exact_sums = !__any_sync(kAll, !exact_sums) && wmax * (double)n * 64.0 < 17592186044416.0;     // 2^44
+    }
+    uint32_t c0 = 0;
+    uint32_t used = 0;                               // names in the on-chip map (warp-uniform)
+    uint64_t* ch_key = s_chkey[wid];
+    uint32_t* ch_mask = s_chmask[wid];
+    int64_t* ch_val = s_chval[wid];
+    const unsigned lt_lanes = (1u << lane) - 1u;
+    for (; a.parallel_pass && exact_sums && c0 < n && used + 32 <= kMapFill; c0 += 32) {
+      const uint32_t cnt = n - c0 < 32 ? n - c0 : 32;
+      const bool live = (uint32_t)lane < cnt;
+      ch_key[lane] = 0; ch_key[lane + 32] = 0; ch_mask[lane] = 0; ch_mask[lane + 32] = 0;
+      uint32_t m = 0;
+      uint64_t op0 = 0, op1 = 0, op2 = 0, op3 = 0, aux = 0;
+      double wgt = 0.0;
+      if (live) {
+        const uint4* src = reinterpret_cast<const uint4*>(ins + c0 + lane);
+        const uint4 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3];
+        m = q0.x;
+        aux = (uint64_t)q1.z | ((uint64_t)q1.w << 32);
+        op0 = (uint64_t)q2.x | ((uint64_t)q2.y << 32); op1 = (uint64_t)q2.z | ((uint64_t)q2.w << 32);
+        op2 = (uint64_t)q3.x | ((uint64_t)q3.y << 32); op3 = (uint64_t)q3.z | ((uint64_t)q3.w << 32);
+        wgt = weight[block_of[c0 + lane]];
+      }
+      const uint32_t cls = ffb_meta_cls(m), nops = ffb_meta_nops(m);
+      const bool is_mem = cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE;
+      // does this statement define a name?  (alignment.py:84-95)
+      bool defines = live && nops >= 1 && ffb_meta_dst_reg(m) && (is_mem ? cls == FFB_CLS_MEMLOAD : ffb_meta_base(m) != FFB_BASE_SETP);
+      const uint64_t dh = ffb_op_hash(op0);
+      __syncwarp();
+      uint32_t my_slot = 0;
+      if (defines) {
+        uint32_t s = slot_of(dh, 64);
+        for (;;) {
+          const unsigned long long prev = atomicCAS((unsigned long long*)&ch_key[s], 0ull, (unsigned long long)(dh + 1));
+          if (prev == 0ull || prev == dh + 1) break;
+          s = (s + 1) & 63u;
+        }
+        atomicOr(&ch_mask[s], 1u << lane);
+        my_slot = s;
+      }
+      __syncwarp();
+      // sources: operands 1..3 and aux
+      SrcScales sc;
+      int p1 = -1, p2 = -1, p3 = -1, pa = -1;
+      unsigned deps = 0;
+#define FFB_RESOLVE(D, S, P)                                                                      \
+      {                                                                                           \
+        const uint64_t kd = ffb_op_kind(D);                                                       \
+        S = kd == FFB_OPK_TIDX ? 1 : ((kd == FFB_OPK_UNKNOWN || kd == FFB_OPK_NONE || kd == FFB_OPK_REG) ? kNoneScale : 0); \
+        if (live && kd == FFB_OPK_REG) {                                                          \
+          const uint64_t h = ffb_op_hash(D);                                                      \
+          uint32_t s = slot_of(h, 64);                                                            \
+          unsigned defs = 0;                                                                      \
+          for (;;) {                                                                              \
+            const uint64_t k = ch_key[s];                                                         \
+            if (k == h + 1) { defs = ch_mask[s] & lt_lanes; break; }                              \
+            if (k == 0) break;                                                                    \
+            s = (s + 1) & 63u;                                                                    \
+          }                                                                                       \
+          if (defs) { P = 31 - __clz((int)defs); deps |= 1u << P; }                               \
+          else S = st.get(h);                                                                     \
+        }                                                                                         \
+      }
+      FFB_RESOLVE(op1, sc.s1, p1)
+      FFB_RESOLVE(op2, sc.s2, p2)
+      FFB_RESOLVE(op3, sc.s3, p3)
+      FFB_RESOLVE(aux, sc.sa, pa)
+#undef FFB_RESOLVE
+      // waves: a statement runs once the lanes it depends on have published
+      bool mine_done = !live;
+      int64_t v = kNoneScale;
+      unsigned done_mask = __ballot_sync(kAll, mine_done);
+      while (done_mask != kAll) {
+        if (!mine_done && (deps & ~done_mask) == 0) {
+          if (p1 >= 0) sc.s1 = ch_val[p1];
+          if (p2 >= 0) sc.s2 = ch_val[p2];
+          if (p3 >= 0) sc.s3 = ch_val[p3];
+          if (pa >= 0) sc.sa = ch_val[pa];
+          if (is_mem) v = ffb_meta_space(m) == FFB_SP_PARAM ? 0 : kNoneScale;            // alignment.py:84-88
+          else if (defines) defines = eval_def(m, op1, op2, op3, sc, &v, &status);
+          if (defines) ch_val[lane] = v;
+          count_statement(m, wgt, sc.sa, acc);
+          mine_done = true;
+        }
+        __syncwarp();
+        done_mask = __ballot_sync(kAll, mine_done);
+      }
+      // the last definer of each name updates the map
+      bool fresh = false;
+      if (defines && (ch_mask[my_slot] >> lane) == 1u) {
+        uint32_t c = slot_of(dh, kMapSlots);
+        for (;;) {
+          const unsigned long long k = st.ckey[c];
+          if (k == dh + 1) break;
+          if (k == 0) {
+            const unsigned long long prev = atomicCAS((unsigned long long*)&st.ckey[c], 0ull, (unsigned long long)(dh + 1));
+            if (prev == 0ull) { fresh = true; break; }
+            if (prev == dh + 1) break;
+          }
+          c = (c + 1) & (kMapSlots - 1);
+        }
+        st.cval[c] = v;
+      }
+      used += __popc(__ballot_sync(kAll, fresh));
+      __syncwarp();
+    }
+    // totals of the parallel part (exact, so the order of the additions does not matter)
+    double n_mem = warp_sum_d(acc.n_mem), mem_bytes = warp_sum_d(acc.mem_bytes), u_fp = warp_sum_d(acc.u_fp), u_int = warp_sum_d(acc.u_int),
+           u_sfu = warp_sum_d(acc.u_sfu), u_alu = warp_sum_d(acc.u_alu), n_sync = warp_sum_d(acc.n_sync);
+    double al_hit = warp_sum_d(acc.al_hit), al_tot = warp_sum_d(acc.al_tot);
+    {
+      unsigned sor = status;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) sor |= __shfl_xor_sync(kAll, sor, d);
+      status = sor;
+    }
+    st.used = used;
+    // sequential remainder (all of the kernel when the parallel form does not apply)
+    for (; c0 < n; c0 += 32) {
       const uint32_t cnt = n - c0 < 32 ? n - c0 : 32;
       if ((uint32_t)lane < cnt) {
         const uint4* src = reinterpret_cast<const uint4*>(ins + c0 + lane);
@@ -631,64 +860,31 @@ flow_kernel(FlowArgs a) {
       }
       __syncwarp();
       if (lane == 0) {
+        Sums sq;
+        sq.n_mem = n_mem; sq.mem_bytes = mem_bytes; sq.u_fp = u_fp; sq.u_int = u_int; sq.u_sfu = u_sfu; sq.u_alu = u_alu;
+        sq.n_sync = n_sync; sq.al_hit = al_hit; sq.al_tot = al_tot;
         for (uint32_t q0 = 0; q0 < cnt; ++q0) {
           const FfbInsRec& r = stage[q0];
-          const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m), base = ffb_meta_base(m);
+          const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m);
           const double wgt = wstage[q0];
           const bool is_mem = cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE;
           if (is_mem) {
-            const uint32_t space = ffb_meta_space(m), bytes = ffb_meta_bytes(m);
-            if (space != FFB_SP_PARAM) { n_mem += wgt; mem_bytes += wgt * (double)bytes; }      // features.py:72-75
-            if (space == FFB_SP_GLOBAL) {                                                      // alignment.py:137-144
-              int64_t sc = kNoneScale;
-              const uint32_t ak = ffb_meta_addr(m);
-              if (ak == FFB_ADDR_SYMBOL) sc = 0;
-              else if (ak == FFB_ADDR_REG) sc = st.get(ffb_op_hash(r.aux));
-              al_tot += wgt;
-              if (sc_known(sc) && sc != kBigScale && (sc < 0 ? -sc : sc) == (int64_t)bytes) al_hit += wgt;
-            }
+            const int64_t sa = (ffb_meta_space(m) == FFB_SP_GLOBAL && ffb_meta_addr(m) == FFB_ADDR_REG) ? st.get(ffb_op_hash(r.aux)) : kNoneScale;
+            count_statement(m, wgt, sa, sq);
             if (cls == FFB_CLS_MEMLOAD && nops >= 1 && ffb_meta_dst_reg(m))                    // alignment.py:84-88
-              st.put(ffb_op_hash(r.op[0]), space == FFB_SP_PARAM ? 0 : kNoneScale);
+              st.put(ffb_op_hash(r.op[0]), ffb_meta_space(m) == FFB_SP_PARAM ? 0 : kNoneScale);
             continue;
           }
-          if (cls == FFB_CLS_FP32) u_fp += wgt;
-          else if (cls == FFB_CLS_INT) u_int += wgt;
-          else if (cls == FFB_CLS_SFU) u_sfu += wgt;
-          else if (cls == FFB_CLS_ALU) u_alu += wgt;
-          else if (cls == FFB_CLS_SYNC) n_sync += wgt;
+          count_statement(m, wgt, kNoneScale, sq);
           if (nops == 0 || !ffb_meta_dst_reg(m)) continue;                                      // alignment.py:91-95
-          const uint64_t dst = ffb_op_hash(r.op[0]);
+          SrcScales sc;
+          sc.s1 = operand_scale_c(r.op[1], st); sc.s2 = operand_scale_c(r.op[2], st);
+          sc.s3 = operand_scale_c(r.op[3], st); sc.sa = operand_scale_c(r.aux, st);
           int64_t v;
-          if (base == FFB_BASE_MOV && nops == 2) v = operand_scale_c(r.op[1], st);
-          else if ((base == FFB_BASE_CVT || base == FFB_BASE_CVTA) && nops >= 2) {
-            uint64_t lastd = nops == 2 ? r.op[1] : nops == 3 ? r.op[2] : nops == 4 ? r.op[3] : r.aux;   // LAST operand
-            if (nops > 5) { status = FFB_E_CAPACITY; lastd = 0; }
-            v = operand_scale_c(lastd, st);
-          } else if ((base == FFB_BASE_ADD || base == FFB_BASE_SUB) && nops == 3) {
-            const int64_t x = operand_scale_c(r.op[1], st), y = operand_scale_c(r.op[2], st);
-            v = base == FFB_BASE_ADD ? sc_add(x, y) : sc_add(x, sc_neg(y));
-          } else if (base == FFB_BASE_MUL && nops == 3) v = mul_scale_c(r.op[1], r.op[2], st);
-          else if ((base == FFB_BASE_MAD || base == FFB_BASE_FMA) && nops == 4)
-            v = sc_add(mul_scale_c(r.op[1], r.op[2], st), operand_scale_c(r.op[3], st));
-          else if (base == FFB_BASE_SHL && nops == 3) {
-            const int64_t x = operand_scale_c(r.op[1], st);
-            if (!sc_known(x) || !is_int_lit(r.op[2])) v = kNoneScale;
-            else {
-              const int64_t sh = int_as_scale(r.op[2]);
-              if (sh == kBigScale || sh < 0) { status = FFB_E_CAPACITY; v = kNoneScale; }   // 1 << huge / negative: reference raises
-              else v = x == 0 ? 0 : (sh >= 61 ? kBigScale : sc_mul(x, (int64_t)1 << sh));
-            }
-          } else if (base == FFB_BASE_SETP) continue;
-          else {
-            // unmodelled producer: uniform only if it has sources and all of them are uniform
-            bool all0 = nops >= 2;
-            for (uint32_t q = 1; q < nops && q < 4 && all0; ++q) all0 = operand_scale_c(r.op[q], st) == 0;
-            if (all0 && nops >= 5) all0 = operand_scale_c(r.aux, st) == 0;
-            if (all0 && nops >= 6 && ffb_meta_extra_reg(m)) { status = FFB_E_CAPACITY; all0 = false; }
-            v = all0 ? 0 : kNoneScale;
-          }
-          st.put(dst, v);
+          if (eval_def(m, r.op[1], r.op[2], r.op[3], sc, &v, &status)) st.put(ffb_op_hash(r.op[0]), v);
         }
+        n_mem = sq.n_mem; mem_bytes = sq.mem_bytes; u_fp = sq.u_fp; u_int = sq.u_int; u_sfu = sq.u_sfu; u_alu = sq.u_alu;
+        n_sync = sq.n_sync; al_hit = sq.al_hit; al_tot = sq.al_tot;
       }
       __syncwarp();
     }
@@ -746,6 +942,7 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   a.ins = (const FfbInsRec*)d->d_ins; a.labels = (const FfbLabelRec*)d->d_labels; a.order = d->d_order;
   a.meta_arr = d->d_meta;
   a.default_trip = d->default_trip;
+  a.parallel_pass = (d->flags & FFB_FLOW_SEQUENTIAL_PASS) ? 0 : 1;
   a.n_ann = d->n_ann > 0 ? d->n_ann : 0; a.ann_hit = d->d_ann_hit;
   a.feat = d->d_feat; a.status = d->d_status; a.flow = d->d_flow;
   a.block_of = (uint32_t*)(base + o_block_of); a.block_start = (uint32_t*)(base + o_bstart);
