@@ -43,6 +43,7 @@ def parse_args():
     ap.add_argument("--kernels", type=int, default=KERNELS_PER_RANK, help="kernels per rank")
     ap.add_argument("--corpus-mb", type=int, default=-1, help="PTX shard per rank in MB (-1: 1250 when the lexer is built)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunk-mb", type=int, default=384, help="chunk size of the overlapped host->device pipeline of the e2e leg")
     ap.add_argument("--lex-flags", type=int, default=0, help="FFB_LEX_* bits for A/B runs (2 = no lock-step CTAs)")
     return ap.parse_args()
 
@@ -185,7 +186,7 @@ def main():
     bufs = {"t": torch.empty((K, 1, J, C), dtype=torch.float64, device=dev),
             "e": torch.empty((K, 1, J, C), dtype=torch.float64, device=dev)}
     if corpus is not None:
-        lex_state = corpus_mod.BenchLexState(rt, corpus)
+        lex_state = corpus_mod.BenchLexState(rt, corpus, chunk_bytes=args.e2e_chunk_mb << 20)
 
     # size the compact front buffer from one untimed, checked pass (inputs are the same every step)
     feat0 = lex_state.run(resident=True) if corpus is not None else d_feat

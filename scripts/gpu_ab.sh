@@ -9,7 +9,7 @@ for f in "$@"; do
   python - <<PY
 import json
 d=json.load(open("gpurun_out/ab_${TAG}_$i.json"))
-print("$f", {k:d[k] for k in ("ms_per_step","phases_ms","ptx_gb_per_s_lexer_only","ptx_gb_per_s_histogram_mode","lexer_segments_fast_exact_slowstmts")})
+print("$f", {k:d[k] for k in ("ms_per_step","phases_ms","ptx_gb_per_s_lexer_only","ptx_gb_per_s_histogram_mode")}, "e2e ms", d["e2e"]["ms_per_step"])
 PY
   i=$((i+1))
 done

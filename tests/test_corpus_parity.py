@@ -278,3 +278,45 @@ def test_parallel_textual_pass_equals_sequential(backend):
         assert np.array_equal(par.status.cpu().numpy(), seq.status.cpu().numpy())
         ok = par.status.cpu().numpy() == 0
         assert par.feat.cpu().numpy()[ok, :11].tobytes() == seq.feat.cpu().numpy()[ok, :11].tobytes()
+
+
+def test_segment_range_calls_equal_whole_corpus(backend):
+    """Chunked pipelines call K1 / K1b on contiguous runs of segments; rows equal the whole-corpus call."""
+    import torch
+    n = 9 if backend == "emul" else 200
+    text, offs = synth.ptx_corpus(seed=31, n_kernels=n, lo=20, hi=300 if backend == "emul" else 3000)
+    corp = corpus.upload_corpus(text, offs)
+    rt = native.get_runtime()
+    lex_all = corpus.lex_records_single_pass(corp)
+    fl_all = corpus.kernel_features(corp, lex_all)
+    lex = corpus.lex_records_single_pass(corp)                      # allocates the buffers (and fills them once)
+    for name in ("hist", "info", "ins", "labels", "meta"):
+        getattr(lex, name).zero_()
+    feat = torch.zeros_like(fl_all.feat)
+    status = torch.full_like(fl_all.status, -1)
+    cuts = [0, n // 3, n // 3 + 1, n]
+    for s0, s1 in zip(cuts[:-1], cuts[1:]):
+        corpus.lex_records_single_pass(corp, out=lex, seg_range=(s0, s1))
+        corpus.kernel_features(corp, lex, out_feat=feat, out_status=status, seg_range=(s0, s1))
+    assert np.array_equal(lex.hist.cpu().numpy(), lex_all.hist.cpu().numpy())
+    assert np.array_equal(lex.info.cpu().numpy(), lex_all.info.cpu().numpy())
+    assert np.array_equal(status.cpu().numpy(), fl_all.status.cpu().numpy())
+    assert feat.cpu().numpy()[:, :11].tobytes() == fl_all.feat.cpu().numpy()[:, :11].tobytes()
+
+
+@pytest.mark.gpu
+def test_streamed_analysis_equals_resident(gpu_only):
+    """StreamedAnalysis (pinned host text, copy overlapped with the kernels) == analyze on resident text."""
+    import torch
+    text, offs = synth.ptx_corpus(seed=33, n_kernels=300, lo=20, hi=3000)
+    corp = corpus.upload_corpus(text, offs)
+    lex, fl = corpus.analyze_corpus(corp)
+    host = torch.empty(corp.padded_bytes, dtype=torch.uint8).pin_memory()
+    host.copy_(corp.text)
+    corp.text.zero_()
+    sa = corpus.StreamedAnalysis(gpu_only, corp, host, chunk_bytes=1 << 20)
+    assert len(sa.bounds) > 3
+    feat = sa.run()
+    torch.cuda.synchronize()
+    assert np.array_equal(sa.status.cpu().numpy(), fl.status.cpu().numpy())
+    assert feat.cpu().numpy()[:, :11].tobytes() == fl.feat.cpu().numpy()[:, :11].tobytes()
