@@ -318,18 +318,18 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     kernels = {
-        "score": {"kernel": "predict_grid_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["score"],
+        "score": {"kernel": "predict_grid_kernel", "ncu_name": "predict_grid_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["score"],
                   "bytes_per_unit": "16 B written per grid point (t_exec, e_pred f64)"},
-        "front": {"kernel": "skyline_group_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["front"],
+        "front": {"kernel": "skyline_group_kernel", "ncu_name": "skyline_group_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["front"],
                   "bytes_per_unit": "16 B read per candidate (e, t f64)"},
     }
     if corpus is not None:
-        kernels["lex"] = {"kernel": "lex_fast_kernel<records>", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
+        kernels["lex"] = {"kernel": "lex_fast_kernel<records>", "ncu_name": "lex_fast_kernel", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
                           "bytes_per_unit": "1 B read per PTX byte (+ ~2 B of records written per byte)"}
-        kernels["lex_hist"] = {"kernel": "lex_fast_kernel<histogram>", "bytes": float(lex_bytes_rank), "ms": hist_ms,
+        kernels["lex_hist"] = {"kernel": "lex_fast_kernel<histogram>", "ncu_name": "lex_fast_kernel_hist", "bytes": float(lex_bytes_rank), "ms": hist_ms,
                                "bytes_per_unit": "1 B read per PTX byte", "in_step": False}
         n_ins = int(lex_state.lex.info_i32()[:, 1].sum().item())
-        kernels["flow"] = {"kernel": "flow_kernel", "bytes": 64.0 * n_ins, "ms": phase_ms["flow"],
+        kernels["flow"] = {"kernel": "flow_kernel", "ncu_name": "flow_kernel", "bytes": 64.0 * n_ins, "ms": phase_ms["flow"],
                            "bytes_per_unit": "64 B read per instruction record"}
     for v in kernels.values():
         v["achieved_gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] > 0 else None
@@ -337,7 +337,11 @@ def main():
     dom = max((k for k in kernels if kernels[k].get("in_step", True)), key=lambda k: kernels[k]["ms"])
     traffic = None
     try:
-        traffic = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(kernels[dom]["kernel"])   # bytes per launch, ncu
+        # dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of that kernel (scripts/summarize_ncu.py);
+        # captured at `kernels_per_launch` kernels per launch, scaled here to this run's launch size (traffic is linear in it)
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(kernels[dom]["ncu_name"])
+        if tr and tr.get("kernels_per_launch"):
+            traffic = tr["dram_bytes_per_launch"] * (K / tr["kernels_per_launch"])
     except (OSError, ValueError):
         pass
     roofline = {"bound": "hbm", "kernel": kernels[dom]["kernel"], "achieved": kernels[dom]["achieved_gbs"], "peak": peak,

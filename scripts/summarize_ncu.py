@@ -67,6 +67,12 @@ def main(tag: str):
             out.append(f"{k:72s} {n:8d} {t*1e3:10.3f} {t/n*1e6:10.1f} {100*t/tot:6.1f}%")
         (OUT / f"launches_{tag}.txt").write_text("\n".join(out) + "\n")
     (OUT / f"traffic_{tag}.json").write_text(json.dumps(traffic, indent=1) + "\n")
+    # bench.py reads profiles/traffic.json: keep the newest capture of every kernel, with the tag it came from
+    latest = OUT / "traffic.json"
+    merged = json.loads(latest.read_text()) if latest.exists() else {}
+    for k, v in traffic.items():
+        merged[k] = {"dram_bytes_per_launch": v, "capture": tag, "kernels_per_launch": int(sys.argv[2]) if len(sys.argv) > 2 else None}
+    latest.write_text(json.dumps(merged, indent=1) + "\n")
     print((OUT / f"ncu_full_{tag}.txt").read_text()[:3000])
 
 
