@@ -78,8 +78,12 @@ FFB_D uint32_t rank2(const uint4* MA, const uint32_t* P, int x) {
 FFB_D uint64_t win64(uint32_t a, uint32_t b, uint32_t c, int sh) {
   return (uint64_t)__funnelshift_r(a, b, sh) | ((uint64_t)__funnelshift_r(b, c, sh) << 32);
 }
-FFB_D uint64_t low_mask(int n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }      // bits [0, n)
-FFB_D uint64_t high_mask(int n) { return n >= 64 ? 0ull : (~0ull << n); }              // bits [n, 64)
+FFB_D uint64_t low_mask(int n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }      // bits [0, n), 0 <= n
+FFB_D uint64_t high_mask(int n) { return n >= 64 ? 0ull : (~0ull << n); }              // bits [n, 64), 0 <= n
+FFB_D uint64_t range_mask(int lo, int hi) {                                            // bits [lo, hi) of a window, any ints
+  lo = lo < 0 ? 0 : lo; hi = hi > 64 ? 64 : hi;
+  return lo >= hi ? 0ull : (low_mask(hi) & high_mask(lo));
+}
 FFB_D uint64_t prefix_xor64(uint64_t x) {
   x ^= x << 1; x ^= x << 2; x ^= x << 4; x ^= x << 8; x ^= x << 16; x ^= x << 32;
   return x;
@@ -445,26 +449,64 @@ FFB_D int classify_plain(const uint8_t* s, int b, int e, int nsemi, int* kb, int
 }
 
 // A line with rare bytes.  s[b,e) is the raw line (scanned whole for "/*"), classification
-// starts at bc >= b (the byte after the kernel's opening brace on that one line).
-FFB_D int resolve_careful(const uint8_t* s, int b, int bc, int e, int* kb, int* ke, bool* slashstar) {
-  int cut = e, ncolon = 0, colon_at = -1, nsemi = 0, run = 0, minrun = 0, nbrace = 0;
-  bool ss = false;
-#pragma unroll 1
-  for (int i = b; i < e; ++i) {
-    const unsigned c = s[i];
-    if (c == '/') {
-      const unsigned c2 = s[i + 1];
-      if (c2 == '*') ss = true;
-      else if (c2 == '/' && cut == e) cut = i;
-    }
-    if (i >= bc && i < cut) {
-      if (c == ';') ++nsemi;
-      else if (c == ':') { if (ncolon++ == 0) colon_at = i; }
-      else if (c == '{') { ++run; ++nbrace; }
-      else if (c == '}') { --run; ++nbrace; if (run < minrun) minrun = run; }
-    }
+// starts at bc >= b (the byte after the kernel's opening brace on that one line).  Only the rare
+// bytes themselves are visited (bits of the line's window of the rare mask); the ';' count comes
+// from the window of the ';' mask.  Lines longer than one window are walked byte by byte.
+struct CarefulScan { int cut, ncolon, colon_at, nsemi, run, minrun, nbrace; bool ss; };
+FFB_D void careful_visit(const uint8_t* s, int i, int bc, int e, CarefulScan& c) {
+  const unsigned ch = s[i];
+  if (ch == '/') {
+    const unsigned c2 = s[i + 1];
+    if (c2 == '*') c.ss = true;
+    else if (c2 == '/' && c.cut == e) c.cut = i;
   }
-  *slashstar = ss;
+  if (i >= bc && i < c.cut) {
+    if (ch == ':') { if (c.ncolon++ == 0) c.colon_at = i; }
+    else if (ch == '{') { ++c.run; ++c.nbrace; }
+    else if (ch == '}') { --c.run; ++c.nbrace; if (c.run < c.minrun) c.minrun = c.run; }
+  }
+}
+FFB_NOINLINE uint64_t careful_scan_bytes(const uint8_t* s, int b, int bc, int e) {     // long lines; returns the packed scan
+  CarefulScan c;
+  c.cut = e; c.ncolon = 0; c.colon_at = -1; c.nsemi = 0; c.run = 0; c.minrun = 0; c.nbrace = 0; c.ss = false;
+  for (int i = b; i < e; ++i) careful_visit(s, i, bc, e, c);
+  for (int i = bc; i < c.cut; ++i) c.nsemi += s[i] == ';' ? 1 : 0;
+  // cut:13 | colon_at+1:13 | flags: ss, ncolon (0,1,2+), nsemi (0,1,2+), brace state (0 none, 1 balanced, 2 bad)
+  const uint32_t bs = c.nbrace == 0 ? 0u : ((c.run == 0 && c.minrun >= 0) ? 1u : 2u);
+  return (uint64_t)c.cut | ((uint64_t)(c.colon_at + 1) << 13) | ((c.ss ? 1ull : 0ull) << 26) | ((uint64_t)(c.ncolon > 2 ? 2 : c.ncolon) << 27) |
+         ((uint64_t)(c.nsemi > 2 ? 2 : c.nsemi) << 29) | ((uint64_t)bs << 31);
+}
+FFB_D int resolve_careful(const uint8_t* s, const uint4* MA, int b, int bc, int e, int* kb, int* ke, bool* slashstar) {
+  int cut, ncolon, colon_at, nsemi;
+  bool braces, balanced;
+  const int n = e - b;
+  if (n <= 128) {                                                // one or two 64-byte windows
+    CarefulScan c;
+    c.cut = e; c.ncolon = 0; c.colon_at = -1; c.nsemi = 0; c.run = 0; c.minrun = 0; c.nbrace = 0; c.ss = false;
+    uint64_t SW0 = 0, SW1 = 0;
+#pragma unroll 1
+    for (int wb = b; wb < e; wb += 64) {
+      const int w0 = wb >> 5, sh = wb & 31, nn = e - wb;
+      const uint4 a0 = MA[w0], a1 = MA[w0 + 1], a2 = MA[w0 + 2];
+      uint64_t RW = win64(a0.y, a1.y, a2.y, sh) & low_mask(nn);
+      const uint64_t SW = win64(a0.x, a1.x, a2.x, sh) & low_mask(nn);
+      if (wb == b) SW0 = SW; else SW1 = SW;
+#pragma unroll 1
+      while (RW) {
+        careful_visit(s, wb + __ffsll((long long)RW) - 1, bc, e, c);
+        RW &= RW - 1;
+      }
+    }
+    cut = c.cut; ncolon = c.ncolon; colon_at = c.colon_at;
+    nsemi = __popcll(SW0 & range_mask(bc - b, cut - b)) + __popcll(SW1 & range_mask(bc - b - 64, cut - b - 64));
+    braces = c.nbrace != 0; balanced = c.run == 0 && c.minrun >= 0;
+    *slashstar = c.ss;
+  } else {
+    const uint64_t r = careful_scan_bytes(s, b, bc, e);
+    cut = (int)(r & 0x1fffu); colon_at = (int)((r >> 13) & 0x1fffu) - 1;
+    *slashstar = ((r >> 26) & 1u) != 0; ncolon = (int)((r >> 27) & 3u); nsemi = (int)((r >> 29) & 3u);
+    braces = ((r >> 31) & 3u) != 0u; balanced = ((r >> 31) & 3u) == 1u;
+  }
   int fb = bc;
 #pragma unroll 1
   while (fb < cut && s[fb] <= ' ') ++fb;
@@ -481,9 +523,9 @@ FFB_D int resolve_careful(const uint8_t* s, int b, int bc, int e, int* kb, int* 
     *ke = lb;
     return FK_LABEL;
   }
-  if (nbrace) {
+  if (braces) {
     if (fb == lb) return s[fb] == '{' ? FK_OPEN : FK_CLOSE;      // ptx.py:237-239
-    if (run != 0 || minrun < 0) return FK_BAD;
+    if (!balanced) return FK_BAD;
   }
   return classify_plain(s, fb, cut, nsemi, kb, ke);
 }
@@ -776,7 +818,7 @@ lex_fast_kernel(LexArgs a) {
           const int b = li == 0 ? lo : nl[li - 1] + 1, e = nl[li];
           const int bc = (li == first && pos > b) ? pos : b;
           bool ss = false;
-          kind = resolve_careful(s, b, bc, e, &kb, &ke, &ss);
+          kind = resolve_careful(s, MA, b, bc, e, &kb, &ke, &ss);
           if (ss && li < ss_line) ss_line = li;
           if (li >= first) {
             linfo[li] = fk_pack(kind, kb, ke);
