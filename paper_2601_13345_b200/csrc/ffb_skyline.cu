@@ -21,6 +21,7 @@
 
 #include <math.h>
 #include <string.h>
+#include <type_traits>
 
 namespace {
 
@@ -49,6 +50,7 @@ struct SkyArgs {
   int resident;             // points staged in shared memory
   int surv_cap;             // survivor capacity (entries of s_pm / s_gs)
   int sort_cap;             // power of two >= surv_cap (entries of s_idx)
+  int surv_bytes;           // bytes of the survivor region: max(surv_cap * 12 for s_pm + s_gs, sort_cap * 8 for the sort keys)
   int tie_smem;             // tie ranks staged in shared memory as u16
   // per-group outputs (optional)
   uint32_t* front_idx;
@@ -144,8 +146,11 @@ skyline_group_kernel(SkyArgs a) {
   double* s_t = s_e + (a.resident ? a.group_size : 0);
   double* s_pm = s_t + (a.resident ? a.group_size : 0);
   uint32_t* s_gs = reinterpret_cast<uint32_t*>(s_pm + MC);
-  IT* s_idx = reinterpret_cast<IT*>(s_gs + MC);
-  uint16_t* s_tie = reinterpret_cast<uint16_t*>(s_idx + a.sort_cap + (a.sort_cap & 1));
+  IT* s_idx = reinterpret_cast<IT*>(reinterpret_cast<unsigned char*>(s_pm) + a.surv_bytes);
+  uint16_t* s_tie = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(s_idx) + (size_t)a.sort_cap * 4);   // slots are 4 B wide
+  // sort keys (ordered bits of e) live where s_pm / s_gs are built after the sort
+  unsigned long long* s_key = reinterpret_cast<unsigned long long*>(s_pm);
+  __shared__ int s_redo;
 
   const double* ge = a.e + p0;
   const double* gt = a.t + p0;
@@ -157,7 +162,7 @@ skyline_group_kernel(SkyArgs a) {
   for (int i = tid; i < G; i += kThreads) {
     const double tv = gt[i];
     if (a.resident) { s_e[i] = ge[i]; s_t[i] = tv; }
-    if (a.tie_smem) s_tie[i] = (uint16_t)a.tie[i];
+    if (a.tie_smem) s_tie[i] = (uint16_t)a.tie[i];          // general sort only
     tmin = tv < tmin ? tv : tmin;
   }
   const double t_peak = block_reduce_min(tmin, s_part);
@@ -210,6 +215,17 @@ skyline_group_kernel(SkyArgs a) {
     if (tid < kBuckets) s_bmin[tid] = excl;
   }
   __syncthreads();
+  auto tie_of = [&](uint32_t i) -> uint64_t {
+    if (a.tie_smem) return s_tie[i];
+    if (a.tie) return a.tie[i];
+    if (a.id) return a.id[p0 + i];
+    return (uint64_t)i;
+  };
+  // packed sort slots: 64-bit key (ordered bits of e) + 32-bit (tie << 16 | index); needs 16-bit indices and ties
+  const bool packed = sizeof(IT) == 2 && a.id == nullptr;
+  uint32_t* s_lo = reinterpret_cast<uint32_t*>(s_idx);
+  if (tid == 0) s_redo = 0;
+  __syncthreads();
   // ---- 4. cull, collect survivors ----
   for (int i0 = 0; i0 < G; i0 += kThreads) {
     const int i = i0 + tid;
@@ -230,7 +246,14 @@ skyline_group_kernel(SkyArgs a) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (keep) {
       const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
-      if (pos < (unsigned)MC) s_idx[pos] = (IT)i;
+      if (pos < (unsigned)MC) {
+        if (packed) {
+          const uint64_t tv = tie_of((uint32_t)i);
+          if (tv > 0xffffull) s_redo = 1;                          // tie rank does not fit: general sort
+          s_lo[pos] = ((uint32_t)tv << 16) | (uint32_t)i;
+          s_key[pos] = (unsigned long long)ordered_bits(pe[i] + 0.0);     // -0.0 == 0.0
+        } else s_idx[pos] = (IT)i;
+      }
     }
   }
   __syncthreads();
@@ -244,16 +267,12 @@ skyline_group_kernel(SkyArgs a) {
   }
   int m2 = 1;
   while (m2 < (int)m_surv) m2 <<= 1;
-  for (int i = m_surv + tid; i < m2; i += kThreads) s_idx[i] = (IT)kPadI;
+  for (int i = m_surv + tid; i < m2; i += kThreads) {
+    if (packed) { s_lo[i] = 0xffffffffu; s_key[i] = ~0ull; } else s_idx[i] = (IT)kPadI;
+  }
   __syncthreads();
 
   // ---- 5. bitonic sort of survivors by (e, t, tie) ----
-  auto tie_of = [&](uint32_t i) -> uint64_t {
-    if (a.tie_smem) return s_tie[i];
-    if (a.tie) return a.tie[i];
-    if (a.id) return a.id[p0 + i];
-    return (uint64_t)i;
-  };
   auto less = [&](uint32_t x, uint32_t y) -> bool {
     if (x == kPadI) return false;
     if (y == kPadI) return true;
@@ -265,34 +284,62 @@ skyline_group_kernel(SkyArgs a) {
   };
   // Stages with partner distance >= 64 synchronise the CTA; the remaining ones (32..1) of a
   // level stay inside 64-element chunks, one warp per chunk, with warp-level barriers only.
-  {
+  auto network = [&](auto cex) {
     const int lane = tid & 31, wid = tid >> 5;
     for (int k = 2; k <= m2; k <<= 1) {
       int j = k >> 1;
       for (; j >= 64; j >>= 1) {
         for (int p = tid; p < (m2 >> 1); p += kThreads) {      // one compare-exchange per pair
           const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
-          const int ixj = i | j;
-          const uint32_t x = s_idx[i], y = s_idx[ixj];
-          const bool asc = (i & k) == 0;
-          if (less(y, x) == asc) { s_idx[i] = (IT)y; s_idx[ixj] = (IT)x; }
+          cex(i, i | j, (i & k) == 0);
         }
         __syncthreads();
       }
       for (int c0 = wid * 64; c0 < m2; c0 += (kThreads / 32) * 64) {
         for (int j2 = j; j2 > 0; j2 >>= 1) {
           const int i = c0 + (((lane & ~(j2 - 1)) << 1) | (lane & (j2 - 1)));
-          const int ixj = i | j2;
-          if (ixj < m2) {
-            const uint32_t x = s_idx[i], y = s_idx[ixj];
-            const bool asc = (i & k) == 0;
-            if (less(y, x) == asc) { s_idx[i] = (IT)y; s_idx[ixj] = (IT)x; }
-          }
+          if ((i | j2) < m2) cex(i, i | j2, (i & k) == 0);
           __syncwarp();
         }
       }
       __syncthreads();
     }
+  };
+  auto cex_general = [&](int i, int ixj, bool asc) {
+    const uint32_t x = s_idx[i], y = s_idx[ixj];
+    if (less(y, x) == asc) { s_idx[i] = (IT)y; s_idx[ixj] = (IT)x; }
+  };
+  if (packed) {
+    // Fast order: (ordered bits of e, tie, index) compared from the slots themselves, no look-ups.  In
+    // the model's grids a tie in e is a tie in t as well (e is a function of t and the cap), so this IS
+    // the (e, t, tie) order; the check below verifies that t never decreases inside a run of equal e
+    // and the sort is redone with the full comparator if it does.
+    auto cex_packed = [&](int i, int ixj, bool asc) {
+      const unsigned long long kx = s_key[i], ky = s_key[ixj];
+      const uint32_t lx = s_lo[i], ly = s_lo[ixj];
+      const bool y_less = ky < kx || (ky == kx && ly < lx);
+      if (y_less == asc && (ky != kx || ly != lx)) { s_key[i] = ky; s_key[ixj] = kx; s_lo[i] = ly; s_lo[ixj] = lx; }
+    };
+    if (!s_redo) network(cex_packed);
+    // slots -> 16-bit indices, in place (every thread reads its slots before anyone writes)
+    // (block by block: the 16-bit index of slot p lands inside slot p/2, which an earlier block owned)
+    for (int base = 0; base < m2; base += kThreads) {
+      const int p = base + tid;
+      const uint32_t v = p < m2 ? s_lo[p] : 0u;
+      __syncthreads();
+      if (p < m2) s_idx[p] = (IT)(v & 0xffffu);
+      __syncthreads();
+    }
+    bool bad = false;                                   // equal e, decreasing t: the (e, tie) order is not (e, t, tie)
+    for (int p = 1 + tid; p < (int)m_surv; p += kThreads) {
+      const uint32_t i = s_idx[p], q = s_idx[p - 1];
+      if (pe[i] == pe[q] && pt[q] > pt[i]) bad = true;
+    }
+    if (bad) s_redo = 1;
+    __syncthreads();
+    if (s_redo) network(cex_general);
+  } else {
+    network(cex_general);
   }
   // ---- 6. exact filter: keep iff t <= min t over strictly lower e ----
   const int m = (int)m_surv;
@@ -351,27 +398,31 @@ skyline_group_kernel(SkyArgs a) {
   }
 }
 
-struct Plan { int resident; int surv_cap; int sort_cap; int tie_smem; size_t smem; };
+struct Plan { int resident; int surv_cap; int sort_cap; int surv_bytes; int tie_smem; size_t smem; };
 
 // Survivor capacity = group size whenever shared memory allows, so a front made of ties
 // (every candidate on it) is still exact; two CTAs per SM stay resident for the 3248-point
 // groups of the headline workload (52 KB of points + 55 KB of survivor arrays).
-Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie) {
+Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie, bool has_id) {
   Plan p;
   const size_t limit = ctx->smem_optin ? ctx->smem_optin - 4096 : 96 * 1024;
   const int64_t idx_bytes = group_size <= 65535 ? 2 : 4;
   auto need = [idx_bytes](int64_t mc, bool resident, int64_t g) {
     int64_t sc = 64; while (sc < mc) sc <<= 1;
-    return (size_t)(mc * 12 + sc * idx_bytes + (resident ? g * 16 : 0) + 64);
+    const int64_t region = ((mc * 12 > sc * 8 ? mc * 12 : sc * 8) + 15) / 16 * 16;
+    return (size_t)(region + sc * 4 + (resident ? g * 16 : 0) + 64);      // 4 B per sort slot: u32 (tie << 16 | index) or IT
   };
   int64_t mc = group_size < 32 ? 32 : group_size;
   p.resident = need(mc, true, group_size) <= limit ? 1 : 0;
   if (!p.resident) { while (mc > 1024 && need(mc, false, group_size) > limit) mc = mc / 2; }
   int64_t sc = 64; while (sc < mc) sc <<= 1;
   p.surv_cap = (int)mc; p.sort_cap = (int)sc;
+  p.surv_bytes = (int)(((mc * 12 > sc * 8 ? mc * 12 : sc * 8) + 15) / 16 * 16);
   p.smem = need(mc, p.resident != 0, group_size);
   p.tie_smem = 0;
-  if (has_tie && p.resident && group_size <= 65535 && p.smem + (size_t)group_size * 2 + 16 <= limit) {
+  // the packed sort reads every survivor's tie exactly once (into its slot): staging the ties would only cost occupancy
+  const bool packed = group_size <= 65535 && !has_id;
+  if (has_tie && !packed && p.resident && group_size <= 65535 && p.smem + (size_t)group_size * 2 + 16 <= limit) {
     p.tie_smem = 1;
     p.smem += (size_t)group_size * 2 + 16;
   }
@@ -379,10 +430,11 @@ Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie) {
 }
 
 int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t stream) {
-  Plan p = plan_groups(ctx, a.group_size, a.tie != nullptr);
+  Plan p = plan_groups(ctx, a.group_size, a.tie != nullptr, a.id != nullptr);
   a.resident = p.resident;
   a.surv_cap = p.surv_cap;
   a.sort_cap = p.sort_cap;
+  a.surv_bytes = p.surv_bytes;
   a.tie_smem = p.tie_smem;
   if (n_groups > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "skyline: too many groups for one launch");
   if (a.group_size <= 65535) {
