@@ -329,19 +329,15 @@ FFB_D double warp_sum_d(double v) {
 // One WARP per kernel.  Lane-parallel: label table, leaders, block numbering, edges, the
 // "last match" scans of the trip recogniser, weights, record staging.  Lane 0 alone: the graph
 // walks (DFS, dominators, loop bodies) and the textual dataflow pass, which are sequential by
-// nature; it reads the records from a 32-entry shared-memory stage the whole warp fills.
-__global__ void __launch_bounds__(kFlowWarps * 32)
+// nature.
+__global__ void __launch_bounds__(kFlowWarps * 32, 5)
 flow_kernel(FlowArgs a) {
-  __shared__ FfbInsRec s_stage[kFlowWarps][32];      // FfbInsRec is 16-byte aligned by declaration
-  __shared__ double s_wstage[kFlowWarps][32];
   __shared__ uint64_t s_ckey[kFlowWarps][kMapSlots];
   __shared__ int64_t s_cval[kFlowWarps][kMapSlots];
   __shared__ uint64_t s_chkey[kFlowWarps][64];      // chunk-local: names the 32 statements in flight define
   __shared__ uint32_t s_chmask[kFlowWarps][64];     //              ... and the lanes that define them
   __shared__ int64_t s_chval[kFlowWarps][32];       //              ... and the values they publish
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  FfbInsRec* stage = s_stage[wid];
-  double* wstage = s_wstage[wid];
 
   for (;;) {
     unsigned long long w = 0;
@@ -852,21 +848,14 @@ flow_kernel(FlowArgs a) {
     // sequential remainder (all of the kernel when the parallel form does not apply)
     for (; c0 < n; c0 += 32) {
       const uint32_t cnt = n - c0 < 32 ? n - c0 : 32;
-      if ((uint32_t)lane < cnt) {
-        const uint4* src = reinterpret_cast<const uint4*>(ins + c0 + lane);
-        uint4* dst = reinterpret_cast<uint4*>(stage + lane);
-        dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2]; dst[3] = src[3];
-        wstage[lane] = weight[block_of[c0 + lane]];
-      }
-      __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) {                                 // (records straight from HBM: this form is the rare one)
         Sums sq;
         sq.n_mem = n_mem; sq.mem_bytes = mem_bytes; sq.u_fp = u_fp; sq.u_int = u_int; sq.u_sfu = u_sfu; sq.u_alu = u_alu;
         sq.n_sync = n_sync; sq.al_hit = al_hit; sq.al_tot = al_tot;
         for (uint32_t q0 = 0; q0 < cnt; ++q0) {
-          const FfbInsRec& r = stage[q0];
+          const FfbInsRec r = ins[c0 + q0];
           const uint32_t m = r.meta, cls = ffb_meta_cls(m), nops = ffb_meta_nops(m);
-          const double wgt = wstage[q0];
+          const double wgt = weight[block_of[c0 + q0]];
           const bool is_mem = cls == FFB_CLS_MEMLOAD || cls == FFB_CLS_MEMSTORE;
           if (is_mem) {
             const int64_t sa = (ffb_meta_space(m) == FFB_SP_GLOBAL && ffb_meta_addr(m) == FFB_ADDR_REG) ? st.get(ffb_op_hash(r.aux)) : kNoneScale;
