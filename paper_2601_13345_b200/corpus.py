@@ -376,7 +376,9 @@ class StreamedAnalysis:
         self.copy_stream = torch.cuda.Stream(device=rt.device) if rt.device.type == "cuda" else None
         self.events = [torch.cuda.Event() for _ in bounds] if self.copy_stream is not None else []
 
-    def run(self, default_trip: float = 32.0) -> torch.Tensor:
+    def run(self, default_trip: float = 32.0, on_chunk=None) -> torch.Tensor:
+        """``on_chunk(c, s0, s1)`` runs on the compute stream right after chunk c's feature rows are
+        enqueued (e.g. to score and rank those kernels while later chunks are still uploading)."""
         rt, corp = self.rt, self.corp
         if self.copy_stream is not None:
             main = torch.cuda.current_stream(rt.device)
@@ -393,6 +395,8 @@ class StreamedAnalysis:
             lex_records_single_pass(corp, out=self.lex, rt=rt, seg_range=(s0, s1), order=self.orders[c])
             kernel_features(corp, self.lex, default_trip=default_trip, out_feat=self.feat, out_status=self.status, rt=rt,
                             seg_range=(s0, s1), order=self.orders[c])
+            if on_chunk is not None:
+                on_chunk(c, s0, s1)
         return self.feat
 
 
@@ -414,14 +418,14 @@ class BenchLexState:
             self.host_text.copy_(self.corp.text)
         return self.host_text
 
-    def run(self, resident: bool = True, mark=None) -> torch.Tensor:
+    def run(self, resident: bool = True, mark=None, on_chunk=None) -> torch.Tensor:
         rt, corp = self.rt, self.corp
         if not resident:
             # host text -> feature rows through the public streamed path: H2D inside the timed
             # region, overlapped chunk by chunk with K1 / K1b
             if self.streamed is None:
                 self.streamed = StreamedAnalysis(rt, corp, self.pin_host(), lex=self.lex, feat=self.feat, chunk_bytes=self.chunk_bytes)
-            self.streamed.run()
+            self.streamed.run(on_chunk=on_chunk)
             if mark is not None:
                 mark.record()
             return self.feat

@@ -46,6 +46,9 @@ struct FfbContext {
   size_t h_stage_cap = 0;
   cudaEvent_t stage_free = nullptr;  // recorded after the last async copy out of h_stage
   bool stage_busy = false;
+  // predict: host copy of the tables that d_tables currently holds (identical inputs skip the upload and its wait)
+  std::vector<unsigned char> tables_shadow;
+  void* tables_shadow_dev = nullptr;
 };
 
 int32_t ffb_fail(FfbContext* ctx, int32_t code, const char* fmt, ...);
