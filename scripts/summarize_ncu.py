@@ -45,7 +45,8 @@ def main(tag: str):
         dur, du = m.get("gpu__time_duration.sum", ("0", "ns"))
         dur_s = float(dur.replace(",", "")) * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(du, 1e-9)
         lines.append(f"{'dram traffic (read+write)':70s} {tr/1e6:16.3f} MB  -> {tr/1e9/max(dur_s,1e-12):.1f} GB/s over {dur_s*1e3:.3f} ms")
-        traffic[name.split('(')[0].split('::')[-1].split('<')[0]] = tr
+        key = name.split('(')[0].split('::')[-1].split('<')[0]
+        traffic[key + ('_hist' if '_hist_' in rep.name else '')] = tr
     (OUT / f"ncu_full_{tag}.txt").write_text("\n".join(lines) + "\n")
     # launch list
     src = ROOT / "gpurun_out" / f"launches_{tag}.csv"
