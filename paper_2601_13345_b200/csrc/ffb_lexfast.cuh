@@ -551,7 +551,7 @@ FFB_D int lane_first(const uint32_t w[4], int lane, int from, int lim, Pred pred
 }
 
 FFB_D bool in_line_comment(const uint8_t* s, int at, int lo) {   // is a "//" open between the line start and `at`?
-  for (int i = at - 2; i >= lo && s[i] != '\n'; --i)
+  for (int i = at - 1; i >= lo && s[i] != '\n'; --i)        // stops at the newline right before `at` too
     if (s[i] == '/' && s[i + 1] == '/') return true;
   return false;
 }

@@ -320,3 +320,33 @@ def test_streamed_analysis_equals_resident(gpu_only):
     torch.cuda.synchronize()
     assert np.array_equal(sa.status.cpu().numpy(), fl.status.cpu().numpy())
     assert feat.cpu().numpy()[:, :11].tobytes() == fl.feat.cpu().numpy()[:, :11].tobytes()
+
+
+def test_long_header_and_launch_shapes(backend):
+    """Kernel headers longer than a tile (the opening brace is found tiles after `.entry`), braces and
+    `.entry` inside header comments; and the fast path's alternative launch shapes (independent CTAs in
+    record mode, barrier-paced CTA in histogram mode) give the same bytes as the default ones."""
+    params = ",\n".join(f"\t.param .u64 a_rather_long_parameter_name_number_{i:04d}" for i in range(160))     # ~8 KB
+    hdr = ("// .entry ghost() {\n.version 8.0\n.visible .entry real_kernel(\n" + params + "\n) // {{{ not yet\n// { nor this\n{\n")
+    body = "".join(f"\tadd.s32 %r{i % 9}, %r{(i + 3) % 9}, {i};\n" for i in range(400))
+    src = hdr + "\t.reg .b32 %r<9>;\n" + body + "\tret;\n}\n"
+    # a comment on the line before the opening brace, and a nested scope the search must not mistake for the body
+    nested = (".visible .entry nest(.param .u64 p) // trailing comment\n{\n\t.reg .b32 %r<4>;\n\tmov.u32 %r1, 1;\n\t{\n"
+              "\tadd.s32 %r1, %r1, 1;\n\t}\n\tret;\n}\n")
+    _check([src, nested])
+    assert corpus.lex_histogram(_corpus([src, nested])).path_counts.cpu().tolist()[:2] == [2, 0]
+    text, offs = synth.ptx_corpus(seed=37, n_kernels=6, lo=20, hi=300)
+    blob = text + src.encode()
+    corp = corpus.upload_corpus(blob, np.concatenate([offs, [len(blob)]]))
+    ref_rec, ref_hist = corpus.lex_records(corp), corpus.lex_histogram(corp)
+    assert ref_rec.path_counts.cpu().tolist()[:2] == [7, 0]
+    for flags in (corpus.LEX_NO_LOCKSTEP, 4):
+        corpus.LEX_FLAGS_DEFAULT = flags
+        try:
+            rec, hist = corpus.lex_records(corp), corpus.lex_histogram(corp)
+        finally:
+            corpus.LEX_FLAGS_DEFAULT = 0
+        for f in ("hist", "info", "ins", "labels", "meta"):
+            assert np.array_equal(getattr(rec, f).cpu().numpy(), getattr(ref_rec, f).cpu().numpy()), (flags, f)
+        assert np.array_equal(hist.hist.cpu().numpy(), ref_hist.hist.cpu().numpy())
+        assert np.array_equal(hist.info.cpu().numpy(), ref_hist.info.cpu().numpy())
