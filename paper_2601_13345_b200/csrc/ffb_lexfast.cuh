@@ -3,7 +3,7 @@
 // finished by exactly one of the two kernels).
 //
 // "Regular" is what compilers emit and what the reference's parse_ptx (ptx.py:207-293) handles
-// without its `pending` machinery: 7-bit text whose only blanks are ' ' '\t' '\n', no "/*"
+// without its `pending` machinery: 7-bit text whose only blanks are ' ' '\t' '\r' '\n', no "/*"
 // anywhere before the end of the kernel body, and body lines that are - after cutting a
 // trailing "// ..." comment (ptx.py:141) - one of
 //     blank | `name:` | bare `{` / `}` | `.directive [;]` | `[@p] opcode operands ;`
@@ -671,7 +671,7 @@ lex_fast_kernel(LexArgs a) {
             n80[j] = ~tn & kH80;
             s80[j] = ~ne80(x, 0x3b3b3b3bu) & kH80;
             r80[j] = ~(ne80(x, 0x3a3a3a3au) & ne80(x, 0x7b7b7b7bu) & ne80(x, 0x7d7d7d7du) & ne80(x, 0x2f2f2f2fu)) & kH80;
-            b80[j] = ~(tt & ne80(x, 0x20202020u)) & kH80;
+            b80[j] = ~(x + 0x5f5f5f5fu) & tn & kH80;          // blank: <= 0x20 and not '\n' (only \t \r ' ' pass the reject test)
             d80[j] = ~ne80(x, 0x2e2e2e2eu) & kH80;
             if (kRecords) {
               const uint32_t y = x | 0x20202020u;              // '[' -> '{', ']' -> '}'
@@ -679,8 +679,9 @@ lex_fast_kernel(LexArgs a) {
               o80[j] = ~(ne80(y, 0x7b7b7b7bu) & ne80(x, 0x28282828u)) & kH80;
               l80[j] = ~(ne80(y, 0x7d7d7d7du) & ne80(x, 0x29292929u)) & kH80;
             }
-            // bytes >= 0x80, and control bytes other than \t \n
-            badacc |= (x & kH80) | (~(x + 0x60606060u) & kH80 & tn & tt);
+            // bytes >= 0x80, and control bytes other than \t \n \r (CR only ever sits in front of a newline or
+            // inside a comment, where Python's strip() / \s treat it like a space)
+            badacc |= (x & kH80) | (~(x + 0x60606060u) & kH80 & tn & tt & ne80(x, 0x0d0d0d0du));
           }
           *reinterpret_cast<uint4*>(s + us) = make_uint4(w[0], w[1], w[2], w[3]);
           reinterpret_cast<uint16_t*>(NLM)[u] = (uint16_t)(pack16(n80[0], n80[1], n80[2], n80[3]) & keep);

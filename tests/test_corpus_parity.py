@@ -157,6 +157,23 @@ def test_fast_path_equals_exact_walk(backend):
         assert np.array_equal(getattr(fast, f).cpu().numpy(), getattr(exact, f).cpu().numpy()), f
 
 
+def test_crlf_text_stays_on_the_fast_path(backend):
+    """CR is a blank for Python's strip() / split() / \\s, so CRLF files (and stray CRs between operands)
+    are regular text: same records as the exact walk, same rows as the oracle, no hand-over."""
+    text, offs = synth.ptx_corpus(seed=41, n_kernels=5, lo=30, hi=250)
+    srcs = [text[offs[i]:offs[i + 1]].decode("ascii").replace("\n", "\r\n") for i in range(5)]
+    srcs[2] = srcs[2].replace(", ", ",\r ", 7).replace(";\r\n", " \r;\r\n", 5)
+    fast, exact = _lex_both(_corpus(srcs))
+    assert fast.path_counts.cpu().tolist()[:2] == [5, 0]
+    for f in ("hist", "info", "ins", "labels", "meta"):
+        assert np.array_equal(getattr(fast, f).cpu().numpy(), getattr(exact, f).cpu().numpy()), f
+    _check(srcs)
+    # CR-only line ends: ONE physical line for the reference (the leading // comment swallows the kernel;
+    # without it the statements share a line)
+    small = ".visible .entry k()\n{\n\t.reg .b32 %r<4>;\n\tmov.u32 %r1, %tid.x;\n\tadd.s32 %r2, %r1, 1;\n\tret;\n}\n"
+    _check([("// c\n" + small).replace("\n", "\r"), small.replace("\n", "\r"), small.replace("\n", "\r\n")])
+
+
 @pytest.mark.parametrize("mutation", ["crlf", "block_comment", "two_statements", "label_and_statement", "multi_line",
                                       "non_ascii", "comment_in_header", "brace_same_line", "trailing_blanks"])
 def test_fast_path_declines_irregular_text(backend, mutation):
