@@ -162,6 +162,15 @@ int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const double* d_t
  * d_id != NULL) of the front in (e, t, id) order.  Syncs (returns the count).
  * d_occ != NULL switches to the 3-objective rule (maximise occupancy as third key):
  * dropped iff some point is strictly better in all three. */
+/* Extension without reference semantics (BASELINE config 5, "3-objective (+occupancy)"): with d_occ given a
+ * candidate is dropped iff another one has strictly lower e, strictly lower t AND occupancy at least as
+ * high; ordering and floor as above.  d_occ == NULL is ffb_skyline_groups.  Capacities: groups of at most
+ * 65535 candidates, at most 64 distinct occupancy values per group (FFB_E_CAPACITY otherwise). */
+int32_t ffb_skyline_groups3(FfbContext* ctx, const double* d_e, const double* d_t, const double* d_occ,
+                            int64_t n_groups, int64_t group_size, const uint32_t* d_tie,
+                            double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
+                            double* d_tpeak, int64_t cap_front, int64_t* d_front_off,
+                            uint32_t* d_status, void* stream);
 int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double* d_t, const double* d_occ,
                     const uint64_t* d_id, int64_t n, double rho, uint64_t* d_front_id,
                     double* d_front_e, double* d_front_t, int64_t cap_front,

@@ -978,6 +978,27 @@ def pareto_indices(e, t, tie=None, rho: float = 0.0):
     return kept, t_peak
 
 
+def pareto_indices3(e, t, occ, tie=None, rho: float = 0.0):
+    """Three-objective EXTENSION (no reference semantics; parity unpinned - this function is the
+    definition the kernel is tested against): after the floor of explorer.py:209-211, candidate i is
+    dropped iff some j has e_j < e_i, t_j < t_i and occ_j >= occ_i.  With a constant occ this is
+    explorer.py:122-140.  O(n^2); order (e, t, tie) as pareto_indices."""
+    e = np.asarray(e, dtype=np.float64)
+    t = np.asarray(t, dtype=np.float64)
+    occ = np.asarray(occ, dtype=np.float64)
+    n = e.size
+    if n == 0:
+        return [], math.inf
+    tie = np.arange(n) if tie is None else np.asarray(tie)
+    t_peak = float(t.min())
+    ok = t <= (t_peak / rho) if rho > 0 else np.ones(n, dtype=bool)
+    idx = np.nonzero(ok & np.isfinite(e) & np.isfinite(t))[0]
+    keep = [int(i) for i in idx if not np.any((e[idx] < e[i]) & (t[idx] < t[i]) & (occ[idx] >= occ[i]))]
+    keep = np.asarray(keep, dtype=np.int64)
+    order = keep[np.lexsort((tie[keep], t[keep], e[keep]))] if keep.size else keep
+    return [int(i) for i in order], t_peak
+
+
 def pareto_bruteforce(e, t):
     """explorer.py:143-158: O(n^2) ground truth (membership only, as a set)."""
     e = np.asarray(e, dtype=np.float64)

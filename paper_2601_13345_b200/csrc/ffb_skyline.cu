@@ -43,6 +43,8 @@ struct SkyArgs {
   const double* e;
   const double* t;
   const uint64_t* id;       // optional per-point id (tie-break + compact output)
+  const double* occ;        // optional third objective (higher is better): see step 6b
+  double* out_occ;          // compact output of occ (hierarchical passes)
   const uint32_t* tie;      // optional [group_size] tie rank
   int64_t n_total;          // total points (last group may be short)
   int64_t group_size;
@@ -236,7 +238,7 @@ skyline_group_kernel(SkyArgs a) {
       if (ok) {
         int b = (int)((ev - emin) * scale);
         b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
-        keep = !(s_bmin[b] < (unsigned long long)ordered_bits(tv));
+        keep = a.occ != nullptr || !(s_bmin[b] < (unsigned long long)ordered_bits(tv));   // the min-t cull ignores occ
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -349,8 +351,78 @@ skyline_group_kernel(SkyArgs a) {
     s_gs[p] = (p == 0 || pe[i] != pe[s_idx[p - 1]]) ? (uint32_t)p : 0u;
   }
   __syncthreads();
-  block_scan_incl(s_pm, m, s_part, MinD(), (double)INFINITY);
+  if (a.occ == nullptr) block_scan_incl(s_pm, m, s_part, MinD(), (double)INFINITY);
   block_scan_incl(s_gs, m, reinterpret_cast<uint32_t*>(s_part), MaxU(), 0u);
+  if (a.occ != nullptr) {
+    // ---- 6b. three objectives (extension, no reference semantics) ----
+    // drop i iff some j has e_j < e_i, t_j < t_i and occ_j >= occ_i.  Occupancy takes few distinct values
+    // (resident warps / max warps), so the test is one prefix-min of t per occupancy level L over the points
+    // with occ >= L, read at the end of the strictly-lower-e prefix.  More than 64 levels: FFB_E_CAPACITY.
+    __shared__ unsigned long long s_lev[64];
+    __shared__ int s_nlev, s_over;
+    uint8_t* s_rank = reinterpret_cast<uint8_t*>(s_idx) + (size_t)a.sort_cap * 2;      // free half of the 4-byte sort slots
+    uint8_t* s_keep = s_rank + a.sort_cap;
+    if (tid < 64) s_lev[tid] = ~0ull;
+    if (tid == 0) { s_nlev = 0; s_over = 0; }
+    __syncthreads();
+    const double* gocc = a.occ + p0;
+    for (int p = tid; p < m; p += kThreads) {
+      const unsigned long long ob = (unsigned long long)ordered_bits(gocc[s_idx[p]] + 0.0);
+      uint32_t sl = (uint32_t)((ob * 0x9E3779B97F4A7C15ull) >> 58);
+      int tries = 0;
+      for (; tries < 64; ++tries) {
+        const unsigned long long prev = atomicCAS(&s_lev[sl], ~0ull, ob);
+        if (prev == ~0ull || prev == ob) break;
+        sl = (sl + 1) & 63u;
+      }
+      if (tries == 64) s_over = 1;
+      s_keep[p] = 1;
+    }
+    __syncthreads();
+    if (s_over) {
+      if (tid == 0) { if (a.front_n) a.front_n[g] = kPad; if (a.status) atomicOr(a.status, 1u << FFB_E_CAPACITY); }
+      return;
+    }
+    if (tid < 32) {                                     // sort the (<= 64) levels ascending, empties last
+      unsigned long long x = s_lev[tid], y = s_lev[tid + 32];
+      for (int k = 2; k <= 64; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          if (j == 32) { if (y < x) { const unsigned long long z = x; x = y; y = z; } }      // asc over the whole 64 (k == 64 only)
+          else {
+            const unsigned long long ox = __shfl_xor_sync(0xffffffffu, x, j), oy = __shfl_xor_sync(0xffffffffu, y, j);
+            const bool lower = (tid & j) == 0;
+            const bool ascx = (tid & k) == 0, ascy = ((tid + 32) & k) == 0;
+            x = (lower == ascx) ? (ox < x ? ox : x) : (ox > x ? ox : x);
+            y = (lower == ascy) ? (oy < y ? oy : y) : (oy > y ? oy : y);
+          }
+        }
+      s_lev[tid] = x; s_lev[tid + 32] = y;
+      const unsigned nx = __ballot_sync(0xffffffffu, x != ~0ull), ny = __ballot_sync(0xffffffffu, y != ~0ull);
+      if (tid == 0) s_nlev = __popc(nx) + __popc(ny);
+    }
+    __syncthreads();
+    const int n_lev = s_nlev;
+    for (int p = tid; p < m; p += kThreads) {
+      const unsigned long long ob = (unsigned long long)ordered_bits(gocc[s_idx[p]] + 0.0);
+      int r = 0;
+      while (s_lev[r] != ob) ++r;
+      s_rank[p] = (uint8_t)r;
+    }
+    __syncthreads();
+    for (int v = 0; v < n_lev; ++v) {
+      for (int p = tid; p < m; p += kThreads) s_pm[p] = s_rank[p] >= v ? pt[s_idx[p]] : (double)INFINITY;
+      __syncthreads();
+      block_scan_incl(s_pm, m, s_part, MinD(), (double)INFINITY);
+      for (int p = tid; p < m; p += kThreads) {
+        if (s_rank[p] != v) continue;
+        const uint32_t gs = s_gs[p];
+        if (gs != 0u && s_pm[gs - 1] < pt[s_idx[p]]) s_keep[p] = 0;
+      }
+      __syncthreads();
+    }
+    for (int p = tid; p < m; p += kThreads) s_gs[p] = s_keep[p];
+    __syncthreads();
+  } else {
   // keep flags -> positions (reuse s_gs after reading the group start)
   for (int p0i = 0; p0i < m; p0i += kThreads) {
     const int p = p0i + tid;
@@ -363,6 +435,7 @@ skyline_group_kernel(SkyArgs a) {
     if (p < m) s_gs[p] = keep;
   }
   __syncthreads();
+  }
   // s_pm no longer needed past this point for p beyond gs lookups: all reads done above
   block_scan_incl(s_gs, m, reinterpret_cast<uint32_t*>(s_part), AddU(), 0u);
   const uint32_t f = m > 0 ? s_gs[m - 1] : 0u;
@@ -393,6 +466,7 @@ skyline_group_kernel(SkyArgs a) {
         a.out_e[obase + rank] = pe[i];
         a.out_t[obase + rank] = pt[i];
         a.out_id[obase + rank] = a.id ? a.id[p0 + i] : (uint64_t)(p0 + i);
+        if (a.out_occ) a.out_occ[obase + rank] = a.occ[p0 + i];
       }
     }
   }
@@ -454,13 +528,24 @@ extern "C" int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const 
                                       double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
                                       double* d_tpeak, int64_t cap_front, int64_t* d_front_off,
                                       uint32_t* d_status, void* stream) {
+  return ffb_skyline_groups3(ctx, d_e, d_t, nullptr, n_groups, group_size, d_tie, rho, d_front_idx, d_front_n, d_tpeak,
+                             cap_front, d_front_off, d_status, stream);
+}
+
+extern "C" int32_t ffb_skyline_groups3(FfbContext* ctx, const double* d_e, const double* d_t, const double* d_occ,
+                                       int64_t n_groups, int64_t group_size, const uint32_t* d_tie,
+                                       double rho, uint32_t* d_front_idx, uint32_t* d_front_n,
+                                       double* d_tpeak, int64_t cap_front, int64_t* d_front_off,
+                                       uint32_t* d_status, void* stream) {
   if (!ctx || !d_e || !d_t || n_groups < 0 || group_size <= 0 || group_size > 0x7fffffffLL || cap_front < 0)
     return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline_groups: bad argument");
+  if (d_occ && group_size > 65535)
+    return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline_groups3: three-objective groups hold at most 65535 candidates");
   if (!(rho <= 1.0)) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline_groups: rho must be <= 1");
   if (n_groups == 0) return FFB_OK;
   FFB_CUDA(ctx, cudaSetDevice(ctx->device));
   SkyArgs a = {};
-  a.e = d_e; a.t = d_t; a.id = nullptr; a.tie = d_tie;
+  a.e = d_e; a.t = d_t; a.occ = d_occ; a.id = nullptr; a.tie = d_tie;
   a.n_total = n_groups * group_size; a.group_size = group_size; a.rho = rho;
   a.front_idx = d_front_idx; a.front_n = d_front_n; a.tpeak = d_tpeak; a.cap_front = cap_front;
   a.status = d_status;
@@ -480,7 +565,6 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
                                int64_t* h_front_n, double* h_tpeak, void* stream_) {
   if (!ctx || !d_e || !d_t || n < 0 || !h_front_n || cap_front <= 0 || !d_front_id)
     return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline: bad argument");
-  if (d_occ) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline: 3-objective fronts are not built yet");
   if (!(rho <= 1.0)) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_skyline: rho must be <= 1");
   cudaStream_t stream = (cudaStream_t)stream_;
   *h_front_n = 0;
@@ -495,13 +579,15 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   int64_t work_cap = n / 8 + 4 * chunk;
   if (work_cap < cap_front) work_cap = cap_front;
   // scratch: two ping-pong triples + counters/status
-  const size_t tri = (size_t)work_cap * 24;
+  const size_t tri = (size_t)work_cap * (d_occ ? 32 : 24);
   int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 2 * tri + 256);
   if (rc) return rc;
   char* base = (char*)ctx->d_sky.p;
   double* buf_e[2] = {(double*)base, (double*)(base + tri)};
   double* buf_t[2] = {buf_e[0] + work_cap, buf_e[1] + work_cap};
   uint64_t* buf_id[2] = {(uint64_t*)(buf_t[0] + work_cap), (uint64_t*)(buf_t[1] + work_cap)};
+  double* buf_occ[2] = {(double*)(buf_id[0] + work_cap), (double*)(buf_id[1] + work_cap)};       // only with d_occ
+  const double* cur_occ = d_occ;
   unsigned long long* d_count = (unsigned long long*)(base + 2 * tri);
   uint32_t* d_status = (uint32_t*)(d_count + 4);
   double* d_tp = (double*)(d_count + 8);
@@ -519,6 +605,9 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
     const int64_t n_groups = (cur_n + chunk - 1) / chunk;
     SkyArgs a = {};
     a.e = cur_e; a.t = cur_t; a.id = cur_id; a.tie = nullptr;
+    a.occ = cur_occ;
+    if (d_occ && (last ? cur_n : chunk) > 65535)
+      return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: the three-objective front does not reduce to one 65535-point group (%lld left)", (long long)cur_n);
     a.n_total = cur_n; a.group_size = last ? cur_n : chunk;
     a.rho = last ? rho : 0.0;
     a.status = d_status;
@@ -529,6 +618,7 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
       a.tpeak = d_tp;
     } else {
       a.out_e = buf_e[which]; a.out_t = buf_t[which]; a.out_id = buf_id[which]; a.out_cap = work_cap;
+      if (d_occ) a.out_occ = buf_occ[which];
     }
     FFB_CUDA(ctx, cudaMemsetAsync(a.out_count, 0, sizeof(unsigned long long), stream));
     rc = launch_groups(ctx, a, last ? 1 : n_groups, stream);
@@ -557,6 +647,7 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
       stalled = true;
     }
     cur_e = buf_e[which]; cur_t = buf_t[which]; cur_id = buf_id[which];
+    if (d_occ) cur_occ = buf_occ[which];
     cur_n = (int64_t)h_count;
     which ^= 1;
   }

@@ -40,9 +40,10 @@ def shard_segments(seg_off: np.ndarray, rank: int, world: int) -> tuple[int, int
 
 
 def merge_fronts(ids: torch.Tensor, e: torch.Tensor, t: torch.Tensor, *, rho: float = 0.0, cap_front: int = 1 << 14,
-                 group=None, rt: native.Runtime | None = None):
+                 group=None, rt: native.Runtime | None = None, occ: torch.Tensor | None = None):
     """All-gather local fronts (padded to ``cap_front``) and run the final skyline pass.
-    Returns (ids, e, t, t_peak) of the global front, identical on every rank."""
+    Returns (ids, e, t, t_peak) of the global front, identical on every rank.  ``occ`` (occupancy of
+    the local front members) switches to the three-objective rule (engine.skyline)."""
     rt = rt or native.get_runtime()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     k = int(ids.numel())
@@ -50,24 +51,31 @@ def merge_fronts(ids: torch.Tensor, e: torch.Tensor, t: torch.Tensor, *, rho: fl
         from .errors import CapacityExceeded
         raise CapacityExceeded(f"local front of {k} points exceeds the exchange capacity {cap_front}")
     inf = float("inf")
-    # one buffer, one collective: [cap, 3] = (e, t, id-as-f64-bits)
-    pack = torch.full((cap_front, 3), inf, dtype=torch.float64, device=rt.device)
+    # one buffer, one collective: [cap, 3 or 4] = (e, t, id-as-f64-bits[, occ])
+    width = 3 if occ is None else 4
+    pack = torch.full((cap_front, width), inf, dtype=torch.float64, device=rt.device)
     pack[:k, 0], pack[:k, 1] = e, t
     pack[:k, 2] = ids.view(torch.float64) if ids.dtype == torch.int64 else ids.to(torch.int64).view(torch.float64)
+    if occ is not None:
+        pack[:, 3] = 0.0                                  # padding rows have e = t = inf and never enter the front
+        pack[:k, 3] = occ
     if world > 1:
-        gathered = torch.empty((world * cap_front, 3), dtype=torch.float64, device=rt.device)
+        gathered = torch.empty((world * cap_front, width), dtype=torch.float64, device=rt.device)
         dist.all_gather_into_tensor(gathered, pack, group=group)
     else:
         gathered = pack
     ge, gt = gathered[:, 0].contiguous(), gathered[:, 1].contiguous()
     gid = gathered[:, 2].contiguous().view(torch.int64)
-    return engine.skyline(ge, gt, ids=gid, rho=rho, cap_front=cap_front, rt=rt)
+    gocc = gathered[:, 3].contiguous() if occ is not None else None
+    return engine.skyline(ge, gt, ids=gid, rho=rho, cap_front=cap_front, rt=rt, occ=gocc)
 
 
 def sharded_skyline(e: torch.Tensor, t: torch.Tensor, first_id: int, *, rho: float = 0.0, cap_front: int = 1 << 14,
-                    group=None, rt: native.Runtime | None = None):
-    """Front of a candidate set whose shard [first_id, first_id + len(e)) lives on this rank."""
+                    group=None, rt: native.Runtime | None = None, occ: torch.Tensor | None = None):
+    """Front of a candidate set whose shard [first_id, first_id + len(e)) lives on this rank
+    (two objectives, or three with ``occ``)."""
     rt = rt or native.get_runtime()
     ids = torch.arange(first_id, first_id + e.numel(), dtype=torch.int64, device=rt.device)
-    lid, le, lt, _ = engine.skyline(e, t, ids=ids, rho=0.0, cap_front=cap_front, rt=rt)   # floor only at the end
-    return merge_fronts(lid, le, lt, rho=rho, cap_front=cap_front, group=group, rt=rt)
+    lid, le, lt, _ = engine.skyline(e, t, ids=ids, rho=0.0, cap_front=cap_front, rt=rt, occ=occ)   # floor only at the end
+    locc = occ[lid - first_id].contiguous() if occ is not None else None
+    return merge_fronts(lid, le, lt, rho=rho, cap_front=cap_front, group=group, rt=rt, occ=locc)

@@ -122,8 +122,9 @@ def enumerate_shapes(spec_row: np.ndarray, shared_dyn: int, dims, rt: native.Run
 def skyline_groups(e: torch.Tensor, t: torch.Tensor, n_groups: int, group_size: int, *,
                    tie: torch.Tensor | None = None, rho: float = 0.95, cap_front: int | None = None,
                    compact: bool = False, out: tuple | None = None, check: bool = True,
-                   rt: native.Runtime | None = None):
-    """K4 on n_groups consecutive groups.
+                   rt: native.Runtime | None = None, occ: torch.Tensor | None = None):
+    """K4 on n_groups consecutive groups.  ``occ`` adds the occupancy objective (extension: a
+    candidate is dropped iff another has strictly lower e and t and occupancy at least as high).
 
     Dense (default): returns (front_idx [n_groups, cap_front], front_n, t_peak).
     ``compact=True``: returns (front_idx [cap_front] flat, front_n, t_peak, front_off) where group
@@ -143,9 +144,11 @@ def skyline_groups(e: torch.Tensor, t: torch.Tensor, n_groups: int, group_size: 
     status = torch.zeros(1, dtype=torch.int32, device=rt.device) if check else None
     if tie is not None:
         assert tie.dtype == torch.int32 and tie.numel() == group_size and tie.is_contiguous()
-    rc = rt.lib.ffb_skyline_groups(rt.ctx, native.ptr(e), native.ptr(t), n_groups, group_size, native.ptr(tie),
-                                   float(rho), native.ptr(front_idx), native.ptr(front_n), native.ptr(tpeak),
-                                   cap_front, native.ptr(front_off), native.ptr(status), rt.stream())
+    if occ is not None:
+        assert occ.dtype == torch.float64 and occ.numel() == e.numel() and occ.is_contiguous()
+    rc = rt.lib.ffb_skyline_groups3(rt.ctx, native.ptr(e), native.ptr(t), native.ptr(occ), n_groups, group_size,
+                                    native.ptr(tie), float(rho), native.ptr(front_idx), native.ptr(front_n),
+                                    native.ptr(tpeak), cap_front, native.ptr(front_off), native.ptr(status), rt.stream())
     rt.check(rc, "ffb_skyline_groups")
     if check:
         st = int(status.item()) & 0xFFFFFFFF
@@ -158,7 +161,7 @@ def skyline_groups(e: torch.Tensor, t: torch.Tensor, n_groups: int, group_size: 
 
 
 def skyline(e: torch.Tensor, t: torch.Tensor, *, ids: torch.Tensor | None = None, rho: float = 0.0,
-            cap_front: int = 1 << 16, rt: native.Runtime | None = None):
+            cap_front: int = 1 << 16, rt: native.Runtime | None = None, occ: torch.Tensor | None = None):
     """K4 on one large candidate set.  Returns (ids, e, t, t_peak) of the front in (e, t, id) order."""
     rt = rt or native.get_runtime()
     assert e.dtype == torch.float64 and t.dtype == torch.float64 and e.is_contiguous() and t.is_contiguous()
@@ -170,7 +173,9 @@ def skyline(e: torch.Tensor, t: torch.Tensor, *, ids: torch.Tensor | None = None
     n_out, tpeak = C.c_int64(0), C.c_double(float("inf"))
     if ids is not None:
         assert ids.dtype == torch.int64 and ids.numel() == n and ids.is_contiguous()
-    rc = rt.lib.ffb_skyline(rt.ctx, native.ptr(e), native.ptr(t), None, native.ptr(ids), n, float(rho),
+    if occ is not None:
+        assert occ.dtype == torch.float64 and occ.numel() == n and occ.is_contiguous()
+    rc = rt.lib.ffb_skyline(rt.ctx, native.ptr(e), native.ptr(t), native.ptr(occ), native.ptr(ids), n, float(rho),
                             native.ptr(out_id), native.ptr(out_e), native.ptr(out_t), cap_front,
                             C.byref(n_out), C.byref(tpeak), rt.stream())
     rt.check(rc, "ffb_skyline")

@@ -51,6 +51,7 @@ _SIGNATURES = {
     "ffb_predict_grid": (_i32, [_vp, C.POINTER(GridDesc), _vp]),
     "ffb_enumerate_shapes": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_i64)]),
     "ffb_skyline_groups": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "ffb_skyline_groups3": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "ffb_lex_corpus": (_i32, [_vp, _vp, _vp]),
     "ffb_kernel_features": (_i32, [_vp, _vp, _vp]),
     "ffb_classify_opcodes": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),

@@ -24,15 +24,18 @@ def _worker(rank: int, world: int, port: int, kind: str, rho: float, out_dir: st
     rt = native.Runtime(native.bind(build_emul()), torch.device("cpu"))
     native.install_runtime_for_tests(rt)
     n = 6000
-    e, t = synth.candidate_cloud(seed=5, n=n, kind=kind)
+    three = kind.endswith("+occ")
+    e, t = synth.candidate_cloud(seed=5, n=n, kind=kind.replace("+occ", ""))
+    occ = (np.random.default_rng(6).integers(1, 6, n) / 5.0) if three else None
     lo, hi = ffd.shard_range(n, rank, world)
     ids, fe, ft, tp = ffd.sharded_skyline(torch.from_numpy(e[lo:hi].copy()), torch.from_numpy(t[lo:hi].copy()), lo,
-                                          rho=rho, cap_front=2048)
+                                          rho=rho, cap_front=2048,
+                                          occ=torch.from_numpy(occ[lo:hi].copy()) if three else None)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids.numpy(), e=fe.numpy(), t=ft.numpy(), tp=tp)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,rho", [("uniform", 0.0), ("tied", 0.9)])
+@pytest.mark.parametrize("kind,rho", [("uniform", 0.0), ("tied", 0.9), ("uniform+occ", 0.0)])
 def test_sharded_front_equals_global_front(tmp_path, kind, rho):
     sys.path.insert(0, str(ROOT / "oracle"))
     import flipflop_oracle as orc
@@ -41,8 +44,12 @@ def test_sharded_front_equals_global_front(tmp_path, kind, rho):
     build_emul()                      # compile once, before the ranks race for it
     port = 29500 + (os.getpid() % 500)
     mp.spawn(_worker, args=(2, port, kind, rho, str(tmp_path)), nprocs=2, join=True)
-    e, t = synth.candidate_cloud(seed=5, n=6000, kind=kind)
-    want, wtp = orc.pareto_indices(e, t, rho=rho)
+    e, t = synth.candidate_cloud(seed=5, n=6000, kind=kind.replace("+occ", ""))
+    if kind.endswith("+occ"):
+        occ = np.random.default_rng(6).integers(1, 6, 6000) / 5.0
+        want, wtp = orc.pareto_indices3(e, t, occ, rho=rho)
+    else:
+        want, wtp = orc.pareto_indices(e, t, rho=rho)
     for r in range(2):
         got = np.load(tmp_path / f"r{r}.npz")
         assert got["ids"].tolist() == want

@@ -123,3 +123,32 @@ def test_front_of_1e9_candidates(gpu_only, kind):
     assert bool(hit.all()) and bool(on_front_or_dominated.all())
     ids2, fe2, ft2, _ = engine.skyline(fe.contiguous(), ft.contiguous(), ids=ids.contiguous(), rho=0.0, cap_front=cap, rt=rt)
     assert torch.equal(ids2, ids) and torch.equal(fe2, fe) and torch.equal(ft2, ft)
+
+
+def test_three_objective_front_of_1e9_candidates(gpu_only):
+    """configs[4], "+occupancy" (extension): 10^9 candidates with 8 occupancy levels.  The 2-objective front is
+    a subset of the 3-objective one (3-objective dominance implies 2-objective dominance), no front member is
+    dominated by another front member, and the front of the front is the front."""
+    rt = gpu_only
+    n = 1_000_000_000
+    g = torch.Generator(device=rt.device).manual_seed(9)
+    e = torch.empty(n, dtype=torch.float64, device=rt.device)
+    t = torch.empty(n, dtype=torch.float64, device=rt.device)
+    occ = torch.empty(n, dtype=torch.float64, device=rt.device)
+    step = 1 << 27
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        e[lo:hi] = torch.rand(hi - lo, generator=g, dtype=torch.float64, device=rt.device) * 10.0
+        t[lo:hi] = torch.rand(hi - lo, generator=g, dtype=torch.float64, device=rt.device) * 10.0
+        occ[lo:hi] = torch.randint(1, 9, (hi - lo,), generator=g, device=rt.device).to(torch.float64) / 8.0
+    cap = 1 << 16
+    ids3, fe3, ft3, _ = engine.skyline(e, t, occ=occ, rho=0.0, cap_front=cap, rt=rt)
+    ids2, fe2, ft2, _ = engine.skyline(e, t, rho=0.0, cap_front=cap, rt=rt)
+    torch.cuda.synchronize()
+    assert 1 <= ids2.numel() <= ids3.numel() < cap
+    assert bool(torch.isin(ids2, ids3).all())
+    fo3 = occ[ids3]
+    dom = (fe3[None, :] < fe3[:, None]) & (ft3[None, :] < ft3[:, None]) & (fo3[None, :] >= fo3[:, None])
+    assert not bool(dom.any())
+    again, *_ = engine.skyline(fe3.contiguous(), ft3.contiguous(), occ=fo3.contiguous(), ids=ids3.contiguous(), rho=0.0, cap_front=cap, rt=rt)
+    assert torch.equal(again, ids3)

@@ -81,3 +81,46 @@ def test_large_set_hierarchical(backend, kind):
     # idempotence: the front of the front is the front
     ids2, *_ = engine.skyline(fe.contiguous(), ft.contiguous(), ids=ids.contiguous(), rho=0.0, cap_front=cap)
     assert ids2.cpu().numpy().tolist() == want
+
+
+@pytest.mark.parametrize("levels,rho", [(1, 0.0), (4, 0.0), (9, 0.9), (64, 0.0)])
+def test_three_objective_groups_match_oracle(backend, levels, rho):
+    """Extension (occupancy as a third objective): groups against the O(n^2) definition in the oracle;
+    one occupancy level reduces to the two-objective front."""
+    rng = np.random.default_rng(100 + levels)
+    n_groups, G = (4, 300) if backend == "emul" else (40, 3248)
+    e = np.round(rng.uniform(0.0, 10.0, n_groups * G), 1)            # rounded: plenty of ties in e and t
+    t = np.round(rng.uniform(1.0, 10.0, n_groups * G), 1)
+    occ = rng.integers(0, levels, n_groups * G).astype(np.float64) / max(levels, 1)
+    tie = rng.permutation(G).astype(np.int32)
+    fi, fn, tp = engine.skyline_groups(_dev(e), _dev(t), n_groups, G, tie=_dev(tie), rho=rho, occ=_dev(occ))
+    fi, fn = fi.cpu().numpy(), fn.cpu().numpy()
+    for g in range(n_groups):
+        sl = slice(g * G, (g + 1) * G)
+        want, wtp = orc.pareto_indices3(e[sl], t[sl], occ[sl], tie=tie, rho=rho)
+        assert fi[g, : int(fn[g])].tolist() == want, (g, levels)
+        assert float(tp[g]) == wtp
+        if levels == 1:
+            assert want == orc.pareto_indices(e[sl], t[sl], tie=tie, rho=rho)[0]
+
+
+def test_three_objective_large_set_and_capacity(backend):
+    n = 20_000 if backend == "emul" else 2_000_000
+    rng = np.random.default_rng(77)
+    e, t = rng.uniform(0.0, 10.0, n), rng.uniform(0.0, 10.0, n)
+    occ = rng.integers(1, 9, n).astype(np.float64) / 8.0
+    ids, fe, ft, tpk = engine.skyline(_dev(e), _dev(t), occ=_dev(occ), rho=0.0, cap_front=1 << 14)
+    want, wtp = [], float(t.min())
+    # reference answer without the O(n^2) scan over everything: a 3-objective front member is a
+    # 2-objective front member of the points whose occupancy is at least its own
+    cand = set()
+    for lv in np.unique(occ):
+        sub = np.nonzero(occ >= lv)[0]
+        cand.update(int(sub[i]) for i in orc.pareto_indices(e[sub], t[sub], rho=0.0)[0])
+    cand = np.asarray(sorted(cand))
+    keep = [int(i) for i in cand if not np.any((e[cand] < e[i]) & (t[cand] < t[i]) & (occ[cand] >= occ[i]))]
+    keep = np.asarray(keep)
+    want = keep[np.lexsort((keep, t[keep], e[keep]))].tolist()
+    assert ids.cpu().numpy().tolist() == want and tpk == wtp
+    with pytest.raises(CapacityExceeded):                  # more than 64 occupancy levels in one group
+        engine.skyline_groups(_dev(e[:4096].copy()), _dev(t[:4096].copy()), 1, 4096, rho=0.0, occ=_dev(rng.uniform(0, 1, 4096)))
