@@ -13,19 +13,25 @@
 // kernel consumes in the same stream.  No host round trip, no CPU path.
 //
 // One warp per segment (dynamic queue), 4 KB tiles:
-//   M  each lane loads eight coalesced 16-byte units and, still in registers, derives 16-bit
-//      position masks by SWAR (newline, ';', "rare" = ':' '{' '}' '/', and '.' while the
-//      kernel header is still being searched) plus a reject flag for bytes outside the
-//      regular alphabet; text and masks go to shared memory (conflict-free 16 B / 2 B stores);
+//   M  each lane loads coalesced 16-byte units and, still in registers, derives 16-bit position
+//      masks by SWAR (newline, ';', "rare" = ':' '{' '}' '/', blank, '.', and in record mode
+//      ',' and opening / closing brackets) plus a reject flag for bytes outside the regular
+//      alphabet; text and masks go to shared memory (conflict-free 16 B / 2 B stores);
 //   T  lane L owns mask words 4L..4L+3: popcounts + one warp scan give the newline table and
 //      per-word prefix counts, so "how many ';' / rare bytes in [b,e)" is two rank queries;
 //   S  `.entry NAME` and the opening '{' by warp-min over mask bits (ptx.py:165-176);
 //   P1 one lane per line: rank queries split lines into plain and careful (any rare byte);
 //      plain lines are classified from first/last byte and the ';' count;
-//      careful lines are compacted and resolved 32 at a time (comment cut, label, braces),
-//      a warp scan of the brace deltas finds the line that closes the body;
-//   P2 one lane per line again: opcode classification / 64-byte records through the same
-//      do_statement the exact kernel uses; record slots come from ballots, not atomics.
+//      careful lines are compacted and resolved 32 at a time, visiting only their rare bytes
+//      (comment cut, label, braces); a warp scan of the brace deltas finds the line that closes
+//      the body;
+//   P2 one lane per statement, parsed from 64-bit windows of the masks: predicate, opcode
+//      tokens (packed words, perfect-hash table), top-level commas, operand spans; operands,
+//      addresses and literals are described from packed 16-byte loads.  Statements the windows
+//      cannot express are compacted and take the byte-serial do_statement of the exact kernel.
+//      Record slots come from ballots, not atomics.
+// Record mode runs as ONE barrier-paced CTA per SM (kLockstep): the warps of a scheduler then run
+// the same phase of this long loop together and share fetched instruction lines.
 #pragma once
 #include "ffb_lex_shared.cuh"
 
