@@ -318,7 +318,33 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
   const int o1 = after ? __ffsll((long long)after) - 1 : n;
   uint64_t D = DT & low_mask(o1) & high_mask(o0);
   uint32_t base = TB_NONE, elem_code = 0, vec = 0, space = 0, cmp = 0, flags = 0;
-  {
+  if (kMode == 1) {
+    // histogram mode needs the class only: the first token, whether the last one is "sync", and - for the
+    // arithmetic bases and sqrt alone - the type / approx tokens in between (ptx.py:104-128)
+    const int t0e = D ? __ffsll((long long)D) - 1 : o1;
+    const int len0 = t0e - o0;
+    base = (len0 > 8 ? 0u : tok_lookup(em.tok, load_packed(s, kb + o0, len0))) & 31u;
+    if (D) {
+      const int ld = 63 - __clzll((long long)D);
+      if (o1 - ld - 1 == 4 && load_packed(s, kb + ld + 1, 4) == ffb_pk("sync")) flags |= 8u;
+      constexpr uint32_t kScan = (1u << TB_ADD) | (1u << TB_SUB) | (1u << TB_MUL) | (1u << TB_MAD) | (1u << TB_FMA) | (1u << TB_DIV) | (1u << TB_SQRT);
+      if ((kScan >> base) & 1u) {
+        int ts = t0e + 1;
+        D &= D - 1;
+#pragma unroll 1
+        for (;;) {
+          const int te = D ? __ffsll((long long)D) - 1 : o1;
+          const int len = te - ts;
+          const uint32_t v = len > 8 ? 0u : tok_lookup(em.tok, load_packed(s, kb + ts, len));
+          flags |= (v >> 8) & 3u;
+          if (v & (1u << 16)) flags |= 4u;
+          if (!D) break;
+          D &= D - 1;
+          ts = te + 1;
+        }
+      }
+    }
+  } else {
     int ts = o0, ti = 0;
     for (;;) {
       const int te = D ? __ffsll((long long)D) - 1 : o1;

@@ -130,11 +130,18 @@ def test_multi_kernel_module_ingestion(backend):
 
 def _lex_both(corp):
     fast = corpus.lex_records(corp)
+    fast_hist = corpus.lex_histogram(corp)
     corpus.EXACT_ONLY_DEFAULT = True
     try:
         exact = corpus.lex_records(corp)
+        exact_hist = corpus.lex_histogram(corp)
     finally:
         corpus.EXACT_ONLY_DEFAULT = False
+    # histogram mode has its own opcode shortcut in the fast path: same histograms and infos as every other way
+    assert np.array_equal(fast_hist.hist.cpu().numpy(), exact_hist.hist.cpu().numpy())
+    assert np.array_equal(fast_hist.info.cpu().numpy(), exact_hist.info.cpu().numpy())
+    ok = exact.info_np()["status"] == 0
+    assert np.array_equal(fast_hist.hist.cpu().numpy()[ok], exact.hist.cpu().numpy()[ok])
     return fast, exact
 
 

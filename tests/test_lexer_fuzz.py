@@ -85,6 +85,7 @@ def test_fast_path_and_exact_walk_agree_on_mutated_kernels(backend, seed):
         exact = corpus.lex_records(corp)
     finally:
         corpus.EXACT_ONLY_DEFAULT = False
+    fast_hist = corpus.lex_histogram(corp)                         # histogram mode: its own opcode shortcut
     taken = fast.path_counts.cpu().tolist()
     assert taken[0] + taken[1] == n and taken[0] > 0            # some of these stay regular
     fi, ei = fast.info_np(), exact.info_np()
@@ -93,6 +94,8 @@ def test_fast_path_and_exact_walk_agree_on_mutated_kernels(backend, seed):
     assert ok.any()
     assert np.array_equal(fast.info.cpu().numpy()[ok], exact.info.cpu().numpy()[ok])
     assert np.array_equal(fast.hist.cpu().numpy()[ok], exact.hist.cpu().numpy()[ok])
+    assert np.array_equal(fast_hist.hist.cpu().numpy()[ok], exact.hist.cpu().numpy()[ok])
+    assert np.array_equal(fast_hist.info.cpu().numpy()[ok], exact.info.cpu().numpy()[ok])
     assert np.array_equal(fast.ins_base.cpu().numpy(), exact.ins_base.cpu().numpy())
     fins, eins = fast.ins.cpu().numpy(), exact.ins.cpu().numpy()
     flab, elab = fast.labels.cpu().numpy(), exact.labels.cpu().numpy()
