@@ -85,7 +85,9 @@ struct FlowArgs {
 
 // ---- tiny open-addressing tables ----------------------------------------------------------------
 // capacities are powers of two
-FFB_D uint32_t slot_of(uint64_t h, uint32_t cap) { return (uint32_t)((h * 0x9E3779B97F4A7C15ull) >> 33) & (cap - 1u); }
+// keys are 61-bit name hashes that went through ffb_hash_fold already (multiply + xorshift): their bits are
+// uniform, so a fold of the two halves is a good slot without another 64-bit multiply
+FFB_D uint32_t slot_of(uint64_t h, uint32_t cap) { return ((uint32_t)h ^ (uint32_t)(h >> 32)) & (cap - 1u); }
 
 struct LabelTable {
   uint64_t* key; uint32_t* first; uint32_t* last; uint32_t cap;
