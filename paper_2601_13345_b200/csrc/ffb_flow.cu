@@ -32,7 +32,8 @@ namespace {
 
 constexpr int kFlowWarps = 4;
 constexpr int kMapSlots = 512;                    // shared-memory register -> scale map per warp (8 KB)
-constexpr int kMapFill = 384;                     // entries kept on chip; later names spill to the HBM table
+constexpr int kMapFill = 384;
+constexpr int kBodyList = 96;                     // loop bodies up to this many blocks are scanned through a compact list                     // entries kept on chip; later names spill to the HBM table
 constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
 constexpr uint32_t kNoBlock = 0xffffffffu;
@@ -338,7 +339,8 @@ flow_kernel(FlowArgs a) {
   __shared__ int64_t s_cval[kFlowWarps][kMapSlots];
   __shared__ uint64_t s_chkey[kFlowWarps][64];      // chunk-local: names the 32 statements in flight define
   __shared__ uint32_t s_chmask[kFlowWarps][64];     //              ... and the lanes that define them
-  __shared__ int64_t s_chval[kFlowWarps][32];       //              ... and the values they publish
+  __shared__ int64_t s_chval[kFlowWarps][32];
+  __shared__ uint32_t s_blist[kFlowWarps][kBodyList];   // blocks of the loop being analysed       //              ... and the values they publish
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   for (;;) {
@@ -548,6 +550,20 @@ flow_kernel(FlowArgs a) {
       if (!is_header) continue;
       __syncwarp();
       const uint32_t h0 = block_start[h];
+      // compact list of the body's blocks: the scans of the trip recogniser visit these only
+      // (bodies with more than kBodyList blocks fall back to testing every block's mark)
+      uint32_t* blist = s_blist[wid];
+      uint32_t n_bl = 0;
+      for (uint32_t b0 = 0; b0 < nb; b0 += 32) {
+        const uint32_t b = b0 + lane;
+        const bool in = b < nb && mark[b] == stamp;
+        const unsigned msk = __ballot_sync(kAll, in);
+        if (in) { const uint32_t at = n_bl + __popc(msk & ((1u << lane) - 1u)); if (at < (uint32_t)kBodyList) blist[at] = b; }
+        n_bl += __popc(msk);
+      }
+      const bool bl_ok = n_bl <= (uint32_t)kBodyList;
+      const uint32_t n_scan = bl_ok ? n_bl : nb;
+      __syncwarp();
       // header label: the dictionary's last name that maps to the header's first instruction
       int64_t best = -1;                        // (first-definition order << 32) | record index
       for (uint32_t i = lane; i < L; i += 32) {
@@ -571,8 +587,9 @@ flow_kernel(FlowArgs a) {
         // cfg.py:191-279; "last match in the body" = maximum index over the body's statements
         bool ok = true;
         int64_t latch = -1;
-        for (uint32_t b = 0; b < nb; ++b) {
-          if (mark[b] != stamp) continue;
+        for (uint32_t bi = 0; bi < n_scan; ++bi) {
+          const uint32_t b = bl_ok ? blist[bi] : bi;
+          if (!bl_ok && mark[b] != stamp) continue;
           for (uint32_t i = block_start[b] + lane; i < block_start[b + 1]; i += 32) {
             const uint32_t m = FFB_META(i);
             if (ffb_meta_cls(m) == FFB_CLS_BRANCH && ffb_meta_has_pred(m)) {
@@ -586,8 +603,9 @@ flow_kernel(FlowArgs a) {
         if (latch < 0) ok = false;
         if (ok) {
           const uint64_t preg = ins[latch].pred;
-          for (uint32_t b = 0; b < nb; ++b) {
-            if (mark[b] != stamp) continue;
+          for (uint32_t bi = 0; bi < n_scan; ++bi) {
+            const uint32_t b = bl_ok ? blist[bi] : bi;
+            if (!bl_ok && mark[b] != stamp) continue;
             for (uint32_t i = block_start[b] + lane; i < block_start[b + 1]; i += 32) {
               const uint32_t m = FFB_META(i);
               if (ffb_meta_base(m) == FFB_BASE_SETP && ffb_meta_nops(m) >= 1) {
@@ -620,8 +638,9 @@ flow_kernel(FlowArgs a) {
           const uint64_t ch = ffb_op_hash(counter);
           int n_upd = 0, n_bad = 0, n_big = 0;
           int64_t my_stride = 0;
-          for (uint32_t b = 0; b < nb; ++b) {
-            if (mark[b] != stamp) continue;
+          for (uint32_t bi = 0; bi < n_scan; ++bi) {
+            const uint32_t b = bl_ok ? blist[bi] : bi;
+            if (!bl_ok && mark[b] != stamp) continue;
             for (uint32_t i = block_start[b] + lane; i < block_start[b + 1]; i += 32) {
               const uint32_t m = FFB_META(i);
               const uint32_t base = ffb_meta_base(m);

@@ -374,3 +374,15 @@ def test_long_header_and_launch_shapes(backend):
             assert np.array_equal(getattr(rec, f).cpu().numpy(), getattr(ref_rec, f).cpu().numpy()), (flags, f)
         assert np.array_equal(hist.hist.cpu().numpy(), ref_hist.hist.cpu().numpy())
         assert np.array_equal(hist.info.cpu().numpy(), ref_hist.info.cpu().numpy())
+
+
+def test_loop_body_larger_than_the_block_list(backend):
+    """A counted loop whose body has ~240 basic blocks (more than the 96-entry on-chip body list of K1b),
+    next to a small one: trips, weights and counts equal the oracle's."""
+    lines = [".visible .entry big_loop(.param .u64 p0)", "{", "\t.reg .b32 %r<9>;", "\t.reg .pred %p<4>;",
+             "\tmov.u32 %r1, 0;", "\tmov.u32 %r5, 3;", "SMALL:", "\tadd.s32 %r5, %r5, 2;", "\tsetp.le.s32 %p3, %r5, 40;", "\t@%p3 bra SMALL;",
+             "LOOP:"]
+    for i in range(120):
+        lines += [f"\tsetp.lt.s32 %p2, %r2, {i};", f"\t@%p2 bra S{i};", "\tadd.s32 %r3, %r3, 1;", f"S{i}:", "\tmul.lo.s32 %r4, %r3, 3;"]
+    lines += ["\tadd.s32 %r1, %r1, 1;", "\tsetp.lt.s32 %p1, %r1, 10;", "\t@%p1 bra LOOP;", "\tret;", "}", ""]
+    _check(["\n".join(lines)])
