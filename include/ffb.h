@@ -246,7 +246,7 @@ typedef struct {
  * path declines are handed over on the device, in the same stream.  FFB_LEX_EXACT_ONLY skips the
  * fast path (it is also skipped for kernel-name filters and span / declaration records). */
 #define FFB_LEX_EXACT_ONLY 1u
-#define FFB_LEX_NO_LOCKSTEP 2u   /* record mode: small independent CTAs instead of one barrier-paced CTA per SM */
+#define FFB_LEX_NO_LOCKSTEP 2u   /* small independent CTAs instead of one barrier-paced CTA per SM (fast path in record mode, exact walk) */
 #define FFB_LEX_LOCKSTEP_HIST 4u /* histogram mode: barrier-paced CTA as well (default: independent CTAs) */
 int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream);
 /* classify_opcode (ptx.py:99) and Instruction.access_bytes (ptx.py:64) for n opcode strings:

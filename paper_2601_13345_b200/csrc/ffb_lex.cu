@@ -121,8 +121,10 @@ FFB_COLD_INLINE LineSummary walk_line(const uint8_t* s, int b, int e, bool pendi
 
 // ---- the kernel --------------------------------------------------------------------------------
 // kRecords: also write FfbInsRec / FfbLabelRec (and the optional span / decl records)
-template <bool kRecords>
-__global__ void __launch_bounds__(kWarps * 32, kRecords ? 2 : 4)   // record mode needs ~128 registers (measured: capping at 64 spills and is 1.5x slower)
+// kLockstep: as in the fast kernel, one CTA fills the SM and its warps meet at a barrier before every tile
+// (the loop body is long; warps of a scheduler that run the same phase share fetched instruction lines).
+template <bool kRecords, bool kLockstep>
+__global__ void __launch_bounds__(kLockstep ? (kRecords ? 512 : 1024) : kWarps * 32, kLockstep ? 1 : (kRecords ? 2 : 4))   // record mode needs ~128 registers (measured: capping at 64 spills and is 1.5x slower)
 lex_corpus_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
@@ -132,49 +134,63 @@ lex_corpus_kernel(LexArgs a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint8_t* s = smem_raw + (size_t)wid * kWarpSmem;
   uint16_t* nl = reinterpret_cast<uint16_t*>(s + kTile + kPad);
-  for (int c = threadIdx.x; c < 256; c += kWarps * 32) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
+  for (int c = threadIdx.x; c < 256; c += (int)blockDim.x) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
   __syncthreads();
-  for (int c = threadIdx.x; c < kNumTokDefs; c += kWarps * 32) {
+  for (int c = threadIdx.x; c < kNumTokDefs; c += (int)blockDim.x) {
     const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
     s_tok_key[slot] = kTokDefs[c].key; s_tok_val[slot] = kTokDefs[c].val;
   }
   __syncthreads();
 
+  // One tile per trip of the main loop: segment state lives across trips so that lock-step CTAs can
+  // meet at a barrier between tiles.
+  bool have = false, done = false, pending = false;                 // pending: ptx.py's `pending` string is non-empty
+  int64_t seg = 0, seg_begin = 0, seg_end = 0, cur = 0;
+  int64_t scan_from_g = 0;                                          // SEARCH / HEADER resume position
+  int64_t body_pos_g = 0;                                           // first body byte (after '{')
+  int64_t noblk_from_g = 0;                                         // from here on "/*" is plain text (unterminated comment)
+  int64_t blk_close_g = -1;                                         // a "*/" is known to exist up to here
+  int64_t name_off = 0, name_len = 0, body_end_off = 0;
+  int phase = PH_SEARCH, depth = 0;
+  int cm_state = S_CODE;                                            // comment automaton state at `cur`
+  uint32_t line_no = 1;                                             // source line of the byte at `cur`
+  uint32_t status = FFB_OK, n_instr = 0, n_labels = 0, n_decls = 0;
+  Emit em;
+  em.a = &a; em.tok.key = s_tok_key; em.tok.val = s_tok_val; em.cls = s_cls;
+  em.seg = 0; em.seg_begin = 0; em.abase = 0; em.line = 0; em.ins_at = 0; em.lab_at = 0;
+  em.ins_limit = 0; em.lab_limit = 0; em.dcl_at = 0; em.c0 = em.c1 = em.c2 = 0;
+  em.shared_bytes = 0; em.regs = 0;
   for (;;) {
+    if (!have && !done) {
     unsigned long long w = 0;
     if (lane == 0) w = atomicAdd(a.work, 1ull);
     w = __shfl_sync(kFull, w, 0);
-    if (w >= (a.n_work ? *a.n_work : (unsigned long long)a.n_segs)) break;
-    const int64_t seg = a.order ? (int64_t)a.order[w] : (int64_t)w;
-    const int64_t seg_begin = a.seg_off[seg], seg_end = a.seg_off[seg + 1];
+    if (w >= (a.n_work ? *a.n_work : (unsigned long long)a.n_segs)) done = true;
+    else {
+      have = true;
+      seg = a.order ? (int64_t)a.order[w] : (int64_t)w;
+      seg_begin = a.seg_off[seg]; seg_end = a.seg_off[seg + 1];
+      phase = PH_SEARCH; cm_state = S_CODE;
+      noblk_from_g = 0x7fffffffffffffffLL; blk_close_g = -1;
+      depth = 0; pending = false; line_no = 1; status = FFB_OK;
+      cur = seg_begin; scan_from_g = seg_begin; body_pos_g = 0;
+      name_off = 0; name_len = 0; body_end_off = 0;
+      n_instr = 0; n_labels = 0; n_decls = 0;
+      em.seg = seg; em.seg_begin = seg_begin; em.abase = 0; em.line = 0;
+      em.ins_at = kRecords ? a.ins_base[seg] : 0;
+      em.lab_at = kRecords ? a.lab_base[seg] : 0;
+      em.ins_limit = (kRecords && a.ins_cap) ? em.ins_at + a.ins_cap[seg] : 0x7fffffffffffffffLL;
+      em.lab_limit = (kRecords && a.lab_cap) ? em.lab_at + a.lab_cap[seg] : 0x7fffffffffffffffLL;
+      em.dcl_at = 0;
+      em.c0 = em.c1 = em.c2 = 0;
+      em.shared_bytes = 0; em.regs = 0;
+    }
+    }
+    if (kLockstep) { if (!__syncthreads_or(done ? 0 : 1)) break; }
+    else if (done) break;
+    if (done) continue;                      // idle warps keep meeting the barrier
 
-    // ---- warp-uniform segment state ----
-    int phase = PH_SEARCH;
-    int cm_state = S_CODE;            // comment automaton state at `cur`
-    int64_t noblk_from_g = 0x7fffffffffffffffLL;   // from here on "/*" is plain text (unterminated comment)
-    int64_t blk_close_g = -1;         // a "*/" is known to exist up to here
-    int depth = 0;
-    bool pending = false;             // ptx.py's `pending` string is non-empty
-    uint32_t line_no = 1;             // source line of the byte at `cur`
-    uint32_t status = FFB_OK;
-    int64_t cur = seg_begin;
-    int64_t scan_from_g = seg_begin;  // SEARCH / HEADER resume position
-    int64_t body_pos_g = 0;           // first body byte (after '{')
-    int64_t name_off = 0, name_len = 0, body_end_off = 0;
-    uint32_t n_instr = 0, n_labels = 0, n_decls = 0;
-
-    Emit em;
-    em.a = &a; em.seg = seg; em.seg_begin = seg_begin; em.abase = 0; em.line = 0;
-    em.tok.key = s_tok_key; em.tok.val = s_tok_val; em.cls = s_cls;
-    em.ins_at = kRecords ? a.ins_base[seg] : 0;
-    em.lab_at = kRecords ? a.lab_base[seg] : 0;
-    em.ins_limit = (kRecords && a.ins_cap) ? em.ins_at + a.ins_cap[seg] : 0x7fffffffffffffffLL;
-    em.lab_limit = (kRecords && a.lab_cap) ? em.lab_at + a.lab_cap[seg] : 0x7fffffffffffffffLL;
-    em.dcl_at = 0;
-    em.c0 = em.c1 = em.c2 = 0;
-    em.shared_bytes = 0; em.regs = 0;
-
-    while (phase != PH_DONE && status == FFB_OK && cur < seg_end) {
+    if (phase != PH_DONE && status == FFB_OK && cur < seg_end) do {
       // ================= T0: stage the tile =================
       const int64_t abase = cur & ~(int64_t)15;
       const int64_t hi_g = (abase + kTile < seg_end) ? abase + kTile : seg_end;
@@ -502,7 +518,9 @@ lex_corpus_kernel(LexArgs a) {
       const int64_t next = abase + consume_to;
       if (next <= cur) { status = FFB_E_CAPACITY; break; }
       cur = next;
-    }
+    } while (0);
+    if (phase != PH_DONE && status == FFB_OK && cur < seg_end) continue;      // more tiles of this segment
+    have = false;
 
     // ================= segment epilogue =================
     if (status == FFB_OK) {
@@ -643,17 +661,22 @@ extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* st
     // the exact kernel takes what the fast path declined (count and list stay on the device)
     a.order = f.fb_list; a.n_work = f.fb_count;
   }
-  const size_t smem = (size_t)kWarps * kWarpSmem;
-  int64_t ctas = (d->n_segs + kWarps - 1) / kWarps;
-  const int64_t max_ctas = (int64_t)ctx->sm_count * 4;
+  // the exact walk is launched barrier-paced as well (one CTA per SM): 16 warps at 128 registers in record mode,
+  // 32 at 64 in histogram mode; FFB_LEX_NO_LOCKSTEP keeps the small independent CTAs
+  const bool xlock = !(d->flags & FFB_LEX_NO_LOCKSTEP);
+  const int xwarps = xlock ? (records ? 16 : 32) : kWarps;
+  const size_t smem = (size_t)xwarps * kWarpSmem;
+  int64_t ctas = (d->n_segs + xwarps - 1) / xwarps;
+  const int64_t max_ctas = xlock ? (int64_t)ctx->sm_count : (int64_t)ctx->sm_count * 4;
   if (ctas > max_ctas) ctas = max_ctas;
-  if (records) {
-    FFB_CUDA(ctx, cudaFuncSetAttribute(lex_corpus_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FFB_LAUNCH(lex_corpus_kernel<true>, (unsigned)ctas, kWarps * 32, smem, stream, a);
-  } else {
-    FFB_CUDA(ctx, cudaFuncSetAttribute(lex_corpus_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FFB_LAUNCH(lex_corpus_kernel<false>, (unsigned)ctas, kWarps * 32, smem, stream, a);
-  }
+#define FFB_LAUNCH_EXACT(R, L)                                                                                           \
+  do {                                                                                                                   \
+    FFB_CUDA(ctx, cudaFuncSetAttribute(lex_corpus_kernel<R, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    FFB_LAUNCH((lex_corpus_kernel<R, L>), (unsigned)ctas, xwarps * 32, smem, stream, a);                                   \
+  } while (0)
+  if (records) { if (xlock) FFB_LAUNCH_EXACT(true, true); else FFB_LAUNCH_EXACT(true, false); }
+  else { if (xlock) FFB_LAUNCH_EXACT(false, true); else FFB_LAUNCH_EXACT(false, false); }
+#undef FFB_LAUNCH_EXACT
   rc = ffb_check_launch(ctx, "lex_corpus_kernel");
   if (rc) return rc;
   if (d->d_path_counts) {

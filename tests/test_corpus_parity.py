@@ -374,6 +374,17 @@ def test_long_header_and_launch_shapes(backend):
             assert np.array_equal(getattr(rec, f).cpu().numpy(), getattr(ref_rec, f).cpu().numpy()), (flags, f)
         assert np.array_equal(hist.hist.cpu().numpy(), ref_hist.hist.cpu().numpy())
         assert np.array_equal(hist.info.cpu().numpy(), ref_hist.info.cpu().numpy())
+    # the exact walk alone, barrier-paced (default) and with independent CTAs
+    irregular = _corpus(list(EDGE_CASES.values()) + [src])
+    outs = []
+    for flags in (0, corpus.LEX_NO_LOCKSTEP):
+        corpus.LEX_FLAGS_DEFAULT, corpus.EXACT_ONLY_DEFAULT = flags, True
+        try:
+            outs.append(corpus.lex_records(irregular))
+        finally:
+            corpus.LEX_FLAGS_DEFAULT, corpus.EXACT_ONLY_DEFAULT = 0, False
+    for f in ("hist", "info", "ins", "labels", "meta"):
+        assert np.array_equal(getattr(outs[0], f).cpu().numpy(), getattr(outs[1], f).cpu().numpy()), f
 
 
 def test_loop_body_larger_than_the_block_list(backend):
