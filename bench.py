@@ -342,10 +342,25 @@ def main():
     value = points_total / (ms_dev / args.steps / 1e3)
     e2e_value = points_total / (ms_e2e / e2e_steps / 1e3)
 
-    # ---- sanity: fronts from the last step are non-empty and ordered ----
+    # ---- sanity: the streamed e2e leg left the same fronts on the HOST as the resident pass computes ----
+    e2e_host = None
+    if e2e.get("regions"):
+        torch.cuda.synchronize()
+        e2e_host = (h_front_n.clone(), h_front_off.clone(), e2e["h_front"].clone())
     _, (fi, fn) = step(True, False)
     torch.cuda.synchronize()
     assert int(fn.min()) >= 1 and int(fn.sum()) == front_total, "fronts changed between steps"
+    if e2e_host is not None:
+        hn, ho, hf = e2e_host
+        assert torch.equal(hn, fn.cpu()), "streamed e2e leg: front sizes differ from the resident pass"
+        fo_res, fi_res = front_bufs[3].cpu(), fi.cpu()
+        bounds = lex_state.streamed.bounds
+        for k in list(range(0, K, max(1, K // 97)))[:128]:                # a sample of kernels, all chunks
+            c = next(i for i, (a0, b0) in enumerate(bounds) if a0 <= k < b0)
+            lo = e2e["regions"][c][0] + int(ho[k])
+            got = hf[lo: lo + int(hn[k])]
+            want = fi_res[int(fo_res[k]): int(fo_res[k]) + int(fn[k])]
+            assert torch.equal(got, want), f"streamed e2e leg: front of kernel {k} differs from the resident pass"
 
     if rank != 0:
         if world > 1:
