@@ -50,9 +50,10 @@ constexpr int kFOffNl = kFOffP + (kFWords + 4) * 4;             // u16[kFMaxLine
 constexpr int kFOffInfo = kFOffNl + (kFMaxLines + 8) * 2;       // u32[kFMaxLines] line info
 constexpr int kFOffMB = kFOffInfo + kFMaxLines * 4;             // record mode: uint4[128 + 4] {comma, open, close, -}
 constexpr int kFWarpSmemHist = kFOffMB;
-constexpr int kFWarpSmemRec = kFOffMB + (kFWords + 4) * 16;
+constexpr int kFOffSort = kFOffMB + (kFWords + 4) * 16;        // record mode: u32[kFMaxLines] statement list being bucketed by length
+constexpr int kFWarpSmemRec = kFOffSort + kFMaxLines * 4;
 static_assert(kFWarpSmemHist % 16 == 0 && kFWarpSmemRec % 16 == 0 && kFOffNlm % 16 == 0 && kFOffMA % 16 == 0 && kFOffP % 16 == 0 &&
-              kFOffInfo % 16 == 0 && kFOffMB % 16 == 0, "smem layout");
+              kFOffInfo % 16 == 0 && kFOffMB % 16 == 0 && kFOffSort % 16 == 0, "smem layout");
 
 enum { FK_BLANK = 0, FK_STMT, FK_LABEL, FK_DIR, FK_DECL, FK_OPEN, FK_CLOSE, FK_BAD };
 constexpr uint32_t kH80 = 0x80808080u;
@@ -880,6 +881,15 @@ lex_fast_kernel(LexArgs a) {
       const uint32_t tile_ins0 = n_instr;
       int n_slow = 0;
       uint16_t* slist = clist;                                   // the careful list is dead by now
+      // Record mode parses the statements of a tile in rounds of SIMILAR LENGTH: a statement's record slot
+      // is fixed by its line order, so the processing order is free, and lines of similar length have
+      // similar token / operand counts - the lanes of a round then follow the same path through the
+      // parser far more often (the union of 32 unrelated statements cost ~4x one statement's path).
+      uint32_t* stmp = reinterpret_cast<uint32_t*>(s + kFOffSort);   // [line] -> slot | bucket << 8 | rank-in-bucket << 16
+      uint16_t* sorted = nl;                                       // the newline table is dead by now
+      uint32_t* bcnt = P;                                          // 32 bucket counters (prefix counts are dead too)
+      if (kRecords) { bcnt[lane] = 0; __syncwarp(); }
+      int n_stmt = 0;
       for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
         const int li = l0 + lane;
         const bool live = li >= first && li < n_eff;
@@ -891,13 +901,21 @@ lex_fast_kernel(LexArgs a) {
         const int64_t my_ins = ins_base + n_instr + __popc(stm & lt_mask);
         bool slow = false;
         if (kind == FK_STMT) {
-          em.ins_at = my_ins;
-          em.line = line_no + (uint32_t)li;
-          slow = !fast_statement<kMain>(s, MA, MB, kb, ke, em);
+          if (kRecords) {
+            const uint32_t bucket = (uint32_t)min((ke - kb) >> 2, 31);
+            const uint32_t r = atomicAdd(&bcnt[bucket], 1u);
+            stmp[li] = (uint32_t)(my_ins - ins_base - tile_ins0) | (bucket << 8) | (r << 16);
+          } else {
+            em.ins_at = my_ins;
+            em.line = line_no + (uint32_t)li;
+            slow = !fast_statement<kMain>(s, MA, MB, kb, ke, em);
+          }
         }
-        const unsigned slm = __ballot_sync(kFull, slow);
-        if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | ((int)(my_ins - ins_base - tile_ins0) << 8));
-        n_slow += __popc(slm);
+        if (!kRecords) {
+          const unsigned slm = __ballot_sync(kFull, slow);
+          if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | ((int)(my_ins - ins_base - tile_ins0) << 8));
+          n_slow += __popc(slm);
+        }
         if (kRecords && kind == FK_LABEL) {
           const int64_t slot = lab_base + n_labels + __popc(lbm & lt_mask);
           FfbLabelRec L;
@@ -914,6 +932,40 @@ lex_fast_kernel(LexArgs a) {
           nd = (int)warp_sum_u64((unsigned long long)nd);
         }
         n_instr += (uint32_t)__popc(stm); n_labels += (uint32_t)__popc(lbm); n_decls += (uint32_t)nd;
+        n_stmt += __popc(stm);
+      }
+      if (kRecords) {
+        __syncwarp();
+        int tot = 0;
+        const uint32_t base_of = (uint32_t)warp_excl_sum((int)bcnt[lane], &tot);    // bucket starts
+        __syncwarp();
+        bcnt[lane] = base_of;
+        __syncwarp();
+        for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
+          const int li = l0 + lane;
+          if (li >= first && li < n_eff && (linfo[li] >> 26) == FK_STMT) {
+            const uint32_t v = stmp[li];
+            sorted[bcnt[(v >> 8) & 31u] + (v >> 16)] = (uint16_t)li;
+          }
+        }
+        __syncwarp();
+        for (int i0 = 0; i0 < n_stmt; i0 += 32) {
+          const int i = i0 + lane;
+          bool slow = false;
+          int li = 0;
+          uint32_t slot = 0;
+          if (i < n_stmt) {
+            li = sorted[i];
+            slot = stmp[li] & 255u;
+            const uint32_t inf = linfo[li];
+            em.ins_at = ins_base + tile_ins0 + slot;
+            em.line = line_no + (uint32_t)li;
+            slow = !fast_statement<kMain>(s, MA, MB, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
+          }
+          const unsigned slm = __ballot_sync(kFull, slow);
+          if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | (slot << 8));
+          n_slow += __popc(slm);
+        }
       }
       __syncwarp();
       n_slow_seg += (uint32_t)n_slow;
