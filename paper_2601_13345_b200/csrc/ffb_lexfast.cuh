@@ -887,8 +887,8 @@ lex_fast_kernel(LexArgs a) {
       // parser far more often (the union of 32 unrelated statements cost ~4x one statement's path).
       uint32_t* stmp = reinterpret_cast<uint32_t*>(s + kFOffSort);   // [line] -> slot | bucket << 8 | rank-in-bucket << 16
       uint16_t* sorted = nl;                                       // the newline table is dead by now
-      uint32_t* bcnt = P;                                          // 32 bucket counters (prefix counts are dead too)
-      if (kRecords) { bcnt[lane] = 0; __syncwarp(); }
+      uint32_t* bcnt = P;                                          // 64 bucket counters (prefix counts are dead too)
+      if (kRecords) { bcnt[lane] = 0; bcnt[lane + 32] = 0; __syncwarp(); }
       int n_stmt = 0;
       for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
         const int li = l0 + lane;
@@ -902,9 +902,9 @@ lex_fast_kernel(LexArgs a) {
         bool slow = false;
         if (kind == FK_STMT) {
           if (kRecords) {
-            const uint32_t bucket = (uint32_t)min((ke - kb) >> 2, 31);
+            const uint32_t bucket = (uint32_t)min(ke - kb, 63);
             const uint32_t r = atomicAdd(&bcnt[bucket], 1u);
-            stmp[li] = (uint32_t)(my_ins - ins_base - tile_ins0) | (bucket << 8) | (r << 16);
+            stmp[li] = (uint32_t)(my_ins - ins_base - tile_ins0) | (bucket << 8) | (r << 16);      // slot 8 bits, bucket 6, rank 9
           } else {
             em.ins_at = my_ins;
             em.line = line_no + (uint32_t)li;
@@ -937,15 +937,16 @@ lex_fast_kernel(LexArgs a) {
       if (kRecords) {
         __syncwarp();
         int tot = 0;
-        const uint32_t base_of = (uint32_t)warp_excl_sum((int)bcnt[lane], &tot);    // bucket starts
+        const uint32_t c0 = bcnt[2 * lane], c1 = bcnt[2 * lane + 1];
+        const uint32_t base_of = (uint32_t)warp_excl_sum((int)(c0 + c1), &tot);     // bucket starts
         __syncwarp();
-        bcnt[lane] = base_of;
+        bcnt[2 * lane] = base_of; bcnt[2 * lane + 1] = base_of + c0;
         __syncwarp();
         for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
           const int li = l0 + lane;
           if (li >= first && li < n_eff && (linfo[li] >> 26) == FK_STMT) {
             const uint32_t v = stmp[li];
-            sorted[bcnt[(v >> 8) & 31u] + (v >> 16)] = (uint16_t)li;
+            sorted[bcnt[(v >> 8) & 63u] + (v >> 16)] = (uint16_t)li;
           }
         }
         __syncwarp();
