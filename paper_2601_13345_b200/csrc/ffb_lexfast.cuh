@@ -50,10 +50,9 @@ constexpr int kFOffNl = kFOffP + (kFWords + 4) * 4;             // u16[kFMaxLine
 constexpr int kFOffInfo = kFOffNl + (kFMaxLines + 8) * 2;       // u32[kFMaxLines] line info
 constexpr int kFOffMB = kFOffInfo + kFMaxLines * 4;             // record mode: uint4[128 + 4] {comma, open, close, -}
 constexpr int kFWarpSmemHist = kFOffMB;
-constexpr int kFOffSort = kFOffMB + (kFWords + 4) * 16;        // record mode: u32[kFMaxLines] statement list being bucketed by length
-constexpr int kFWarpSmemRec = kFOffSort + kFMaxLines * 4;
+constexpr int kFWarpSmemRec = kFOffMB + (kFWords + 4) * 16;
 static_assert(kFWarpSmemHist % 16 == 0 && kFWarpSmemRec % 16 == 0 && kFOffNlm % 16 == 0 && kFOffMA % 16 == 0 && kFOffP % 16 == 0 &&
-              kFOffInfo % 16 == 0 && kFOffMB % 16 == 0 && kFOffSort % 16 == 0, "smem layout");
+              kFOffInfo % 16 == 0 && kFOffMB % 16 == 0, "smem layout");
 
 enum { FK_BLANK = 0, FK_STMT, FK_LABEL, FK_DIR, FK_DECL, FK_OPEN, FK_CLOSE, FK_BAD };
 constexpr uint32_t kH80 = 0x80808080u;
@@ -881,13 +880,14 @@ lex_fast_kernel(LexArgs a) {
       const uint32_t tile_ins0 = n_instr;
       int n_slow = 0;
       uint16_t* slist = clist;                                   // the careful list is dead by now
-      // Record mode parses the statements of a tile in rounds of SIMILAR LENGTH: a statement's record slot
-      // is fixed by its line order, so the processing order is free, and lines of similar length have
+      // Record mode parses the statements of a tile in rounds of SIMILAR LENGTH (histogram mode, whose parser
+      // is short, loses more to the sort than it gains: 416 -> 388 GB/s, so it keeps line order): a statement's record slot is
+      // fixed by its line order, so the processing order is free, and lines of the same length have
       // similar token / operand counts - the lanes of a round then follow the same path through the
-      // parser far more often (the union of 32 unrelated statements cost ~4x one statement's path).
-      uint32_t* stmp = reinterpret_cast<uint32_t*>(s + kFOffSort);   // [line] -> slot | bucket << 8 | rank-in-bucket << 16
-      uint16_t* sorted = nl;                                       // the newline table is dead by now
-      uint32_t* bcnt = P;                                          // 64 bucket counters (prefix counts are dead too)
+      // parser far more often (the union of 32 unrelated statements costs ~4x one statement's path).
+      // Counting sort by length: histogram, scan, scatter of (line | slot << 8) into the dead newline table.
+      uint16_t* sorted = nl;
+      uint32_t* bcnt = P;                                          // 64 bucket counters (the prefix counts are dead too)
       if (kRecords) { bcnt[lane] = 0; bcnt[lane + 32] = 0; __syncwarp(); }
       int n_stmt = 0;
       for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
@@ -899,19 +899,14 @@ lex_fast_kernel(LexArgs a) {
         const unsigned lbm = __ballot_sync(kFull, kind == FK_LABEL);
         const unsigned dcm = __ballot_sync(kFull, kind == FK_DECL);
         const int64_t my_ins = ins_base + n_instr + __popc(stm & lt_mask);
-        bool slow = false;
-        if (kind == FK_STMT) {
-          if (kRecords) {
-            const uint32_t bucket = (uint32_t)min(ke - kb, 63);
-            const uint32_t r = atomicAdd(&bcnt[bucket], 1u);
-            stmp[li] = (uint32_t)(my_ins - ins_base - tile_ins0) | (bucket << 8) | (r << 16);      // slot 8 bits, bucket 6, rank 9
-          } else {
+        if (kRecords) { if (kind == FK_STMT) atomicAdd(&bcnt[min(ke - kb, 63)], 1u); }
+        else {
+          bool slow = false;
+          if (kind == FK_STMT) {
             em.ins_at = my_ins;
             em.line = line_no + (uint32_t)li;
             slow = !fast_statement<kMain>(s, MA, MB, kb, ke, em);
           }
-        }
-        if (!kRecords) {
           const unsigned slm = __ballot_sync(kFull, slow);
           if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | ((int)(my_ins - ins_base - tile_ins0) << 8));
           n_slow += __popc(slm);
@@ -934,39 +929,45 @@ lex_fast_kernel(LexArgs a) {
         n_instr += (uint32_t)__popc(stm); n_labels += (uint32_t)__popc(lbm); n_decls += (uint32_t)nd;
         n_stmt += __popc(stm);
       }
+      __syncwarp();
       if (kRecords) {
-        __syncwarp();
         int tot = 0;
         const uint32_t c0 = bcnt[2 * lane], c1 = bcnt[2 * lane + 1];
         const uint32_t base_of = (uint32_t)warp_excl_sum((int)(c0 + c1), &tot);     // bucket starts
         __syncwarp();
         bcnt[2 * lane] = base_of; bcnt[2 * lane + 1] = base_of + c0;
         __syncwarp();
+        uint32_t seen = 0;
         for (int l0 = first & ~31; l0 < n_eff; l0 += 32) {
           const int li = l0 + lane;
-          if (li >= first && li < n_eff && (linfo[li] >> 26) == FK_STMT) {
-            const uint32_t v = stmp[li];
-            sorted[bcnt[(v >> 8) & 63u] + (v >> 16)] = (uint16_t)li;
+          const bool live = li >= first && li < n_eff;
+          const uint32_t inf = live ? linfo[li] : 0u;
+          const bool st = (int)(inf >> 26) == FK_STMT;
+          const unsigned stm = __ballot_sync(kFull, st);
+          if (st) {
+            const uint32_t slot = seen + __popc(stm & lt_mask);                      // statement index within the tile
+            const uint32_t at = atomicAdd(&bcnt[min((int)((inf >> 13) & 0x1fffu) - (int)(inf & 0x1fffu), 63)], 1u);
+            sorted[at] = (uint16_t)(li | (slot << 8));
           }
+          seen += __popc(stm);
         }
         __syncwarp();
-        for (int i0 = 0; i0 < n_stmt; i0 += 32) {
-          const int i = i0 + lane;
-          bool slow = false;
-          int li = 0;
-          uint32_t slot = 0;
-          if (i < n_stmt) {
-            li = sorted[i];
-            slot = stmp[li] & 255u;
-            const uint32_t inf = linfo[li];
-            em.ins_at = ins_base + tile_ins0 + slot;
-            em.line = line_no + (uint32_t)li;
-            slow = !fast_statement<kMain>(s, MA, MB, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
-          }
-          const unsigned slm = __ballot_sync(kFull, slow);
-          if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | (slot << 8));
-          n_slow += __popc(slm);
+      }
+      for (int i0 = 0; kRecords && i0 < n_stmt; i0 += 32) {
+        const int i = i0 + lane;
+        bool slow = false;
+        uint32_t ent = 0;
+        if (i < n_stmt) {
+          ent = sorted[i];
+          const int li = (int)(ent & 255u);
+          const uint32_t inf = linfo[li];
+          em.ins_at = ins_base + tile_ins0 + (ent >> 8);
+          em.line = line_no + (uint32_t)li;
+          slow = !fast_statement<kMain>(s, MA, MB, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
         }
+        const unsigned slm = __ballot_sync(kFull, slow);
+        if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)ent;
+        n_slow += __popc(slm);
       }
       __syncwarp();
       n_slow_seg += (uint32_t)n_slow;
