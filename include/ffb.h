@@ -247,7 +247,7 @@ typedef struct {
  * fast path (it is also skipped for kernel-name filters and span / declaration records). */
 #define FFB_LEX_EXACT_ONLY 1u
 #define FFB_LEX_NO_LOCKSTEP 2u   /* small independent CTAs instead of one barrier-paced CTA per SM (fast path in record mode, exact walk) */
-#define FFB_LEX_LOCKSTEP_HIST 4u /* histogram mode: barrier-paced CTA as well (default: independent CTAs) */
+#define FFB_LEX_LOCKSTEP_HIST 4u /* accepted and ignored: histogram mode is barrier-paced by default as well */
 int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* stream);
 /* classify_opcode (ptx.py:99) and Instruction.access_bytes (ptx.py:64) for n opcode strings:
  * string i is d_text[d_off[i] : d_off[i+1]); d_out[n,3] = {class, state space, access bytes}. */

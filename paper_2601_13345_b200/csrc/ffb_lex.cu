@@ -640,9 +640,9 @@ extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* st
     f.fb_count = (unsigned long long*)ctx->d_lex.p + 1;
     f.fb_list = (int32_t*)((uint8_t*)ctx->d_lex.p + 4096);
     // lock-step shape: one CTA per SM (16 warps at 128 registers in record mode, 24 at 80 in histogram mode)
-    // measured (r1p): 17.1 ms vs 32.0 ms per 1.44 GB in record mode; histogram mode has a short loop and
-    // loses 3% to the barrier, so it keeps small independent CTAs unless asked otherwise
-    const bool lockstep = records ? !(d->flags & FFB_LEX_NO_LOCKSTEP) : (d->flags & FFB_LEX_LOCKSTEP_HIST) != 0;
+    // measured: record mode 17.1 ms vs 32.0 ms per 1.44 GB (r1p); histogram mode 482 vs 416 GB/s once its
+    // parser had been shortened (r1z; before that the barrier cost it 3%)
+    const bool lockstep = !(d->flags & FFB_LEX_NO_LOCKSTEP);
     const int fwarps = lockstep ? (records ? 16 : 24) : kFWarps;
     const size_t fsmem = (size_t)fwarps * (records ? kFWarpSmemRec : kFWarpSmemHist);
     int64_t fctas = (d->n_segs + fwarps - 1) / fwarps;

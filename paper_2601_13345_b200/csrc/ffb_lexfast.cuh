@@ -30,8 +30,8 @@
 //      addresses and literals are described from packed 16-byte loads.  Statements the windows
 //      cannot express are compacted and take the byte-serial do_statement of the exact kernel.
 //      Record slots come from ballots, not atomics.
-// Record mode runs as ONE barrier-paced CTA per SM (kLockstep): the warps of a scheduler then run
-// the same phase of this long loop together and share fetched instruction lines.
+// Both modes run as ONE barrier-paced CTA per SM (kLockstep): the warps of a scheduler then run the
+// same phase of this long loop together and share fetched instruction lines.
 #pragma once
 #include "ffb_lex_shared.cuh"
 
