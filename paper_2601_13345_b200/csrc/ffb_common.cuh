@@ -49,6 +49,7 @@ struct FfbContext {
   // predict: host copy of the tables that d_tables currently holds (identical inputs skip the upload and its wait)
   std::vector<unsigned char> tables_shadow;
   void* tables_shadow_dev = nullptr;
+  void* tables_shadow_stream = nullptr;   // the upload is only known to be ordered before work on this stream
 };
 
 int32_t ffb_fail(FfbContext* ctx, int32_t code, const char* fmt, ...);

@@ -375,7 +375,7 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
       return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "shape %lld: block dims must be >= 1", (long long)j);
     h_log[j] = fabs(log((double)bx / (double)by));                             // power_model.py:61
   }
-  if (!(ctx->tables_shadow_dev == ctx->d_tables.p && ctx->tables_shadow.size() == bytes &&
+  if (!(ctx->tables_shadow_dev == ctx->d_tables.p && ctx->tables_shadow_stream == (void*)stream && ctx->tables_shadow.size() == bytes &&
         memcmp(ctx->tables_shadow.data(), scratch.data(), bytes) == 0)) {
     rc = ffb_stage_reserve(ctx, bytes);
     if (rc) return rc;
@@ -385,6 +385,7 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
     ctx->stage_busy = true;
     ctx->tables_shadow.swap(scratch);
     ctx->tables_shadow_dev = ctx->d_tables.p;
+    ctx->tables_shadow_stream = (void*)stream;
   }
   Tables tb;
   double* d = (double*)ctx->d_tables.p;
