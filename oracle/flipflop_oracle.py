@@ -784,17 +784,50 @@ def _pmax(a, b):
     return b if b > a else a
 
 
+def occupancy_ext(arch: dict, bx: int, by: int, bz: int = 1, regs: int = 0, regs_per_sm: int = 0,
+                  shared: int = 0):
+    """Occupancy of one block shape, with the two EXTENSION axes north_star (2) names and the
+    reference does not define (it records registers, features.py:126, and never limits on them;
+    LaunchConfig has no block_z, launch.py:11-21) - "parity unpinned", this function IS the definition:
+
+      threads = bx*by*bz;  warps = threads // 32                      (features.py:96,110 with z)
+      bps = max_warps / warps                                          (features.py:112)
+      if shared > 0:  bps = min(bps, max_shared / shared)              (features.py:113-114)
+      if regs_per_sm > 0 and regs > 0:                                 (extension)
+          bps = min(bps, regs_per_sm / (regs * threads))      registers a resident block needs
+      valid iff 32 <= threads <= max_threads, threads % 32 == 0, warps <= max_warps and, with a
+      register limit, regs_per_sm / (regs * threads) >= 1.0           (explorer.py:79-88 style)
+
+    With bz = 1 and regs_per_sm = 0 every line is the reference's.  Returns (valid, warps, bps)."""
+    threads = bx * by * bz
+    if threads < 32 or threads > arch["max_threads_per_block"] or threads % 32:
+        return False, 0, 0.0
+    warps = threads // 32
+    bps = arch["max_warps_per_sm"] / warps
+    valid = warps <= arch["max_warps_per_sm"]
+    if shared > 0:
+        bps = _pmin(bps, arch["max_shared_per_sm"] / shared)
+    if regs_per_sm > 0 and regs > 0:
+        lim = float(regs_per_sm) / float(regs * threads)
+        bps = _pmin(bps, lim)
+        valid = valid and lim >= 1.0
+    return valid, warps, bps
+
+
 def score_point(feat, arch: dict, cal: dict, bx: int, by: int, cap: float, shared_dyn: int,
-                total_blocks: int):
+                total_blocks: int, bz: int = 1, regs: int = 0, regs_per_sm: int = 0):
     """features.py:96-114, time_model.py:67-129, power_model.py:124-170, explorer.py:105-108.
     feat: dict with n_mem, mem_bytes, FP32, INT, SFU, ALU, n_sync, aligned, static_shared.
+    bz / regs / regs_per_sm: extension axes, see occupancy_ext (defaults = the reference).
     Returns dict(t_exec, p_dyn, e_pred, cap_limited, blocks_per_sm, warps, eta)."""
-    threads = bx * by
+    threads = bx * by * bz
     warps = threads // 32
     shared = int(feat["static_shared"]) + shared_dyn
     bps = arch["max_warps_per_sm"] / warps
     if shared > 0:
         bps = _pmin(bps, arch["max_shared_per_sm"] / shared)
+    if regs_per_sm > 0 and regs > 0:
+        bps = _pmin(bps, float(regs_per_sm) / float(regs * threads))
     eta = _pmin(1.0, bx / 32.0) * feat["aligned"]
     resident = _pmin(bps * warps, float(arch["max_warps_per_sm"]))
     lanes = arch["sm_count"] * resident * 32.0
@@ -870,26 +903,35 @@ def enumerate_configs(arch: dict, shared_dyn: int, dims, caps=None):
 
 
 def score_grid_numpy(feat_rows: np.ndarray, res_rows: np.ndarray, arch: dict, cal: dict,
-                     shapes: np.ndarray, caps: np.ndarray):
+                     shapes: np.ndarray, caps: np.ndarray, regs_per_sm: int = 0, return_occ: bool = False):
     """Vectorised score_point over kernels x shapes x caps for ONE spec (numpy elementwise
     ops are the same IEEE operations as the scalar code, in the same order).
-    feat_rows [K, >=9] (FFB_F_* order), res_rows [K,2], shapes [J,2] valid shapes.
-    Returns t, e as [K,J,C]."""
+    feat_rows [K, >=9] (FFB_F_* order), res_rows [K,2], shapes [J,2] valid shapes, or [J,4]
+    {bx, by, bz, regs} with the extension axes of occupancy_ext.
+    Returns t, e as [K,J,C] (and blocks_per_sm [K,J] with return_occ)."""
     f = np.asarray(feat_rows, dtype=np.float64)
     K = f.shape[0]
+    shapes = np.asarray(shapes)
     bx = shapes[:, 0].astype(np.int64)[None, :]
     by = shapes[:, 1].astype(np.int64)[None, :]
+    bz = shapes[:, 2].astype(np.int64)[None, :] if shapes.shape[1] > 2 else np.ones_like(bx)
+    regs = shapes[:, 3].astype(np.int64)[None, :] if shapes.shape[1] > 3 else np.zeros_like(bx)
     n_mem, mem_bytes = f[:, 0:1], f[:, 1:2]
     u = {"FP32": f[:, 2:3], "INT": f[:, 3:4], "SFU": f[:, 4:5], "ALU": f[:, 5:6]}
     n_sync, aligned = f[:, 6:7], f[:, 7:8]
     shared = (f[:, 8].astype(np.int64) + res_rows[:, 0])[:, None]
     total_blocks = res_rows[:, 1][:, None]
-    warps = (bx * by) // 32
+    warps = (bx * by * bz) // 32
     wf = warps.astype(np.float64)
     bps = np.broadcast_to(arch["max_warps_per_sm"] / wf, (K, wf.shape[1])).copy()
     with np.errstate(divide="ignore"):
         lim = np.where(shared > 0, arch["max_shared_per_sm"] / np.maximum(shared, 1).astype(np.float64), np.inf)
     bps = np.where(lim < bps, lim, bps)
+    if regs_per_sm > 0:
+        need = (regs * bx * by * bz).astype(np.float64)
+        with np.errstate(divide="ignore"):
+            rlim = np.where(regs > 0, float(regs_per_sm) / np.maximum(need, 1.0), np.inf)
+        bps = np.where(rlim < bps, rlim, bps)
     r = bx / 32.0
     eta = np.where(r < 1.0, r, 1.0) * aligned
     mw = float(arch["max_warps_per_sm"])
@@ -928,7 +970,7 @@ def score_grid_numpy(feat_rows: np.ndarray, res_rows: np.ndarray, arch: dict, ca
         if ex <= 0:
             continue
         p_units = p_units + cal["beta_u"][name] * (cnt * wps / (ex / arch["issue_cycles"][name]))
-    logs = np.array([abs(math.log(int(x) / int(y))) for x, y in shapes], dtype=np.float64)[None, :]
+    logs = np.array([abs(math.log(int(x) / int(y))) for x, y in shapes[:, :2]], dtype=np.float64)[None, :]
     with np.errstate(invalid="ignore", divide="ignore"):
         ci = n_comp / n_mem
         p_shape = np.where(n_mem == 0, cal["p_base_shape"],
@@ -949,6 +991,8 @@ def score_grid_numpy(feat_rows: np.ndarray, res_rows: np.ndarray, arch: dict, ca
     p_dyn = np.where(over, np.where(room > 0.0, room, 0.0), p_dyn)
     t3 = np.broadcast_to(t_exec[:, :, None], p_dyn.shape)
     e = t3 * (p_dyn + arch["p_static"]) + cal["e_overhead"]
+    if return_occ:
+        return np.ascontiguousarray(t3), e, np.ascontiguousarray(bps)
     return np.ascontiguousarray(t3), e
 
 

@@ -19,7 +19,7 @@ from .api import (  # noqa: F401
     activity_rate, analyze_memory_alignment, build_cfg, classify_opcode, coalescing_efficiency,
     compute_input_resources, compute_intensity, cwp, dvfs_frequency, dynamic_instruction_counts, dynamic_power,
     estimate_active_sms, estimate_trip_counts, evaluate_configs, execution_time, extract_features,
-    generate_valid_configs, memory_power, mwp, pareto_explore, pareto_front, pareto_front_bruteforce, parse_ptx,
+    generate_valid_configs, memory_power, mwp, pareto_explore, pareto_explore_sweep, pareto_front, pareto_front_bruteforce, parse_ptx,
     predict_energy, shape_power, sm_concurrency_power, transient_correction, wave_count,
 )
 

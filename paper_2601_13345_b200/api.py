@@ -64,9 +64,14 @@ _PARAM = re.compile(r"\.param\s+(?:\.align\s+\d+\s+)?\.(\w+)\s+([\w$]+)(?:\[(\d+
 
 
 def _header_parameters(src: bytes, name: str, name_off: int, body_off: int) -> tuple:
-    """Kernel parameter list (ptx.py:190-204): header metadata, not consumed by any model."""
-    header = _clean_span(src[name_off: max(body_off - 1, name_off)]) if b"/" in src[name_off:body_off] \
-        else src[name_off: max(body_off - 1, name_off)].decode("utf-8", "replace")
+    """Kernel parameter list (ptx.py:190-204): header metadata, not consumed by any model.
+    The header runs from the LAST `.entry` before the body (ptx.py:191, rfind) to the opening brace,
+    on the comment-stripped text (ptx.py:139-141)."""
+    head = src[:body_off].decode("utf-8", "replace")
+    if "/" in head:
+        head = re.sub(r"/\*.*?\*/", lambda m: re.sub(r"[^\n]", " ", m.group(0)), head, flags=re.S)
+        head = re.sub(r"//[^\n]*", "", head)
+    header = head[max(head.rfind(".entry"), 0):]
     lp = header.find("(")
     if lp < 0:
         return ()
@@ -162,6 +167,12 @@ def _handle_of(module: PtxModule) -> _KernelHandle:
         return module._dev
     # a hand-built module: serialise it back to PTX and lex that on the device
     lines = [f".entry {module.kernel_name}()", "{"]
+    # declarations carry numbers the models read (features.py:111 static shared, :126 registers)
+    for n_decl, (cls, count) in enumerate(module.registers_declared.items()):
+        tag = "".join(chr(ord("a") + int(d)) for d in str(n_decl))          # register names are letters only (ptx.py:37)
+        lines.append(f".reg .{cls} %ffbdecl_{tag}<{int(count)}>;")
+    if module.static_shared_bytes:
+        lines.append(f".shared .b8 ffb_static_shared[{int(module.static_shared_bytes)}];")
     by_index: dict[int, list[str]] = {}
     for name, idx in module.labels.items():
         by_index.setdefault(idx, []).append(name)
@@ -490,6 +501,9 @@ def evaluate_configs(module: PtxModule, cfg: ControlFlowGraph, arch: Architectur
     out = []
     for c in configs:
         d = det[s_idx[(c.block_x, c.block_y)], c_idx[float(c.p_cap)]]
+        if not (math.isfinite(d[_N.D_T_EXEC]) and math.isfinite(d[_N.D_E_PRED])):
+            # IEEE gives inf / nan where CPython raises (a zero divisor such as ipc = 0, time_model.py:116)
+            raise ZeroDivisionError("float division by zero")
         out.append(Prediction(config=c, time=_time_of(d), power=_power_of(d), e_pred=float(d[_N.D_E_PRED])))
     out.sort(key=lambda p: _config_key(p.config))
     return out
@@ -504,10 +518,19 @@ def _front_order(predictions: list[Prediction], rho: float):
     tie = np.empty(n, dtype=np.int32)
     tie[keys] = np.arange(n, dtype=np.int32)
     rt = native.get_runtime()
-    fi, fn, tp = engine.skyline_groups(rt.to_device(torch.from_numpy(e)), rt.to_device(torch.from_numpy(t)), 1, n,
-                                       tie=rt.to_device(torch.from_numpy(tie)), rho=rho, cap_front=n, rt=rt)
-    k = int(fn.cpu()[0])
-    return fi.cpu().numpy()[0, :k].tolist(), float(tp.cpu()[0])
+    d_e, d_t = rt.to_device(torch.from_numpy(e)), rt.to_device(torch.from_numpy(t))
+    try:
+        fi, fn, tp = engine.skyline_groups(d_e, d_t, 1, n, tie=rt.to_device(torch.from_numpy(tie)), rho=rho, cap_front=n, rt=rt)
+        k = int(fn.cpu()[0])
+        return fi.cpu().numpy()[0, :k].tolist(), float(tp.cpu()[0])
+    except CapacityExceeded:
+        # the front does not fit one CTA's shared memory (e.g. > 10^4 mutually non-dominated points):
+        # the streaming skyline takes any size; ids carry the tie rank so the order is still (e, t, bx, by, cap)
+        inv = np.empty(n, dtype=np.int64)
+        inv[tie] = np.arange(n)
+        ids, _, _, t_peak = engine.skyline(d_e, d_t, ids=rt.to_device(torch.from_numpy(tie.astype(np.int64))), rho=rho,
+                                           cap_front=n, rt=rt)
+        return inv[ids.cpu().numpy()].tolist(), float(t_peak)
 
 
 def pareto_front(predictions: list[Prediction]) -> list[Prediction]:
@@ -538,3 +561,59 @@ def pareto_explore(module: PtxModule, cfg: ControlFlowGraph, arch: ArchitectureS
     predictions = evaluate_configs(module, cfg, arch, profile, resources, configs, jobs=jobs)
     idx, t_peak = _front_order(predictions, float(rho))
     return ParetoSet(entries=tuple(predictions[i] for i in idx), rho=rho, t_peak=t_peak)
+
+
+def pareto_explore_sweep(module: PtxModule, cfg: ControlFlowGraph, specs: list, resources: list[InputResources],
+                         dim_candidates: list[int], cap_candidates: list[float], rho: float = 0.95) -> dict:
+    """Per-spec, per-workload fronts from ONE grid launch and ONE skyline launch (the
+    paper's per-sequence-length fronts).  ``specs`` is a list of (ArchitectureSpec,
+    CalibrationProfile); ``resources`` a list of InputResources (e.g. compute_input_resources per
+    seq_len).  Returns {(spec_index, resource_index): ParetoSet}; every entry equals
+    ``pareto_explore(module, cfg, arch, profile, resources[r], dim_candidates, cap_candidates, rho)``
+    (explorer.py:186-212), or the NoFeasibleConfig instance it would raise."""
+    if not 0 < rho <= 1:
+        raise ValueError(f"rho must be in (0, 1], got {rho}")
+    if not cap_candidates:
+        raise ValueError("the sweep needs an explicit cap list (the default cap is spec-dependent)")
+    rt = native.get_runtime()
+    row = _feature_row(module, cfg)
+    caps = sorted({float(c) for c in cap_candidates})
+    sp = engine.spec_rows(specs)
+    # shape axis: union over specs (validity is masked per point on the device); canonical order is spec-independent
+    seen = {}
+    for s in range(len(specs)):
+        for bx, by in engine.enumerate_shapes(sp[s], 0, dim_candidates, rt=rt).tolist():
+            seen[(bx, by)] = None
+    shapes = sorted(seen, key=lambda x: (x[0] * x[1], x[0], x[1]))
+    if not shapes:
+        return {(s, r): NoFeasibleConfig("no candidate configuration passed the hardware filters")
+                for s in range(len(specs)) for r in range(len(resources))}
+    J, Cn, S, R = len(shapes), len(caps), len(specs), len(resources)
+    res_axis = torch.tensor([[r.shared_mem_bytes, r.total_blocks] for r in resources], dtype=torch.int64)
+    g = engine.score_grid_sweep(engine.features_tensor([row]), rt.to_device(res_axis), sp, engine.shape_rows(shapes),
+                                np.asarray(caps), want=("t", "e", "flags", "detail"), rt=rt)
+    order = sorted(range(J), key=lambda j: (shapes[j][0], shapes[j][1]))
+    rank = np.empty(J, dtype=np.int64)
+    rank[order] = np.arange(J)
+    tie = (rank[:, None] * Cn + np.arange(Cn)[None, :]).reshape(-1).astype(np.int32)
+    G = J * Cn
+    fi, fn, tp = engine.skyline_groups(g.e.reshape(-1), g.t.reshape(-1), R * S, G, tie=rt.to_device(torch.from_numpy(tie)),
+                                       rho=float(rho), cap_front=G, rt=rt)
+    fi, fn, tp = fi.cpu().numpy(), fn.cpu().numpy(), tp.cpu().numpy()
+    det = g.detail.cpu().numpy().reshape(R * S, G, _N.DETAIL_WIDTH)
+    valid = (g.flags.cpu().numpy().reshape(R * S, G) & _N.PT_VALID) != 0
+    out = {}
+    for r in range(R):
+        for s in range(S):
+            q = r * S + s
+            if not valid[q].any():
+                out[(s, r)] = NoFeasibleConfig("no candidate configuration passed the hardware filters")
+                continue
+            entries = []
+            for i in fi[q, : int(fn[q])]:
+                j, c = divmod(int(i), Cn)
+                d = det[q, i]
+                conf = LaunchConfig(block_x=shapes[j][0], block_y=shapes[j][1], p_cap=caps[c])
+                entries.append(Prediction(config=conf, time=_time_of(d), power=_power_of(d), e_pred=float(d[_N.D_E_PRED])))
+            out[(s, r)] = ParetoSet(entries=tuple(entries), rho=rho, t_peak=float(tp[q]))
+    return out

@@ -436,22 +436,6 @@ class BenchLexState:
         return self.feat
 
 
-def smoke_check(rt: native.Runtime) -> None:
-    """One small corpus through K1 + K1b on the GPU, compared with the oracle."""
-    import flipflop_oracle as orc           # test infrastructure, only reachable from smoke()
-    from . import synth
-    text, offs = synth.ptx_corpus(seed=2, n_kernels=24, lo=30, hi=400)
-    corp = upload_corpus(text, offs, rt=rt)
-    lex, fl = analyze_corpus(corp, rt=rt)
-    hist, feat, status = lex.hist.cpu().numpy(), fl.feat.cpu().numpy(), fl.status.cpu().numpy()
-    for k in range(corp.n_segs):
-        src = text[offs[k]:offs[k + 1]].decode("ascii")
-        kern = orc.parse_kernel(src)
-        assert status[k] == 0 and hist[k].tolist() == orc.class_histogram(kern), f"histogram differs (kernel {k})"
-        want = np.asarray(orc.kernel_feature_row(src), dtype=np.float64)
-        assert feat[k, :11].tobytes() == want.tobytes(), f"feature row differs (kernel {k})"
-
-
 # ------------------------------------------------------------------------------ multi-kernel modules
 def split_modules(text: bytes, module_off: np.ndarray | None = None, *, max_kernels_per_module: int = 1 << 16,
                   rt: native.Runtime | None = None) -> Corpus:

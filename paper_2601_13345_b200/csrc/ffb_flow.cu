@@ -8,11 +8,11 @@
 // %tid.x scale map, single textual pass) and :128-147 (weighted aligned fraction),
 // features.py:62-81 (dynamic counts).
 //
-// One THREAD per kernel: the analysis is a chain of sequential, data-dependent walks over a
-// few hundred to a few thousand 64-byte records, so the parallelism is across the tens of
-// thousands of kernels of a corpus (threads of a warp take neighbouring entries of the
-// longest-first order, i.e. kernels of similar length).  All working arrays live in a
-// context-owned HBM scratch indexed by the same exclusive scans as the records.
+// One WARP per kernel (dynamic queue, longest first).  Lane-parallel: label table, leaders, block
+// numbering, edges, predecessor lists, the "last match" scans of the trip recogniser, weights and
+// the textual dataflow pass (32 statements per round).  Lane 0 alone: DFS, dominators and loop
+// bodies, which are sequential graph walks.  The CFG working arrays live in a context-owned HBM
+// scratch indexed by the same exclusive scans as the records.
 //
 // Dominators: the reference iterates full bit-sets to the maximal fixed point.  For blocks
 // reachable from block 0 that equals the dominator tree (computed here with the

@@ -100,6 +100,7 @@ struct GridArgs {
   Tables tb;
   int64_t n_units;     // K*S*J
   int n_specs, n_shapes, n_caps;
+  int cap_tile;        // caps staged per pass (== n_caps unless the [units, caps] tile would not fit shared memory)
   double* t;
   double* e;
   double* pdyn;
@@ -112,22 +113,29 @@ struct GridArgs {
 
 // kLean: only t / e requested and no strict checks — the streaming configuration
 template <bool kDetail, bool kLean>
-__global__ void __launch_bounds__(kUnitsPerCta)
+__global__ void __launch_bounds__(kUnitsPerCta, kLean ? 5 : 1)
 predict_grid_kernel(GridArgs a) {
   FFB_DYN_SMEM(smem_raw);
-  const int C = a.n_caps;
-  double* s_t = reinterpret_cast<double*>(smem_raw);            // [units][C]
-  double* s_e = s_t + (size_t)kUnitsPerCta * C;
-  double* s_p = s_e + (size_t)kUnitsPerCta * C;                 // only when pdyn requested
-  uint8_t* s_f = reinterpret_cast<uint8_t*>(s_p + (a.pdyn ? (size_t)kUnitsPerCta * C : 0));
+  const int C = a.n_caps, CT = a.cap_tile;
+  double* s_t = reinterpret_cast<double*>(smem_raw);            // [units][CT]
+  double* s_e = s_t + (size_t)kUnitsPerCta * CT;
+  double* s_p = s_e + (size_t)kUnitsPerCta * CT;                // only when pdyn requested
+  uint8_t* s_f = reinterpret_cast<uint8_t*>(s_p + (a.pdyn ? (size_t)kUnitsPerCta * CT : 0));
 
   const int64_t unit0 = (int64_t)blockIdx.x * kUnitsPerCta;
   const int64_t unit = unit0 + threadIdx.x;
   const bool live = unit < a.n_units;
 
+  // per-thread values the cap axis needs (set by live threads only)
+  double t_exec = 0.0, p_pre = 0.0, p_static = 0.0, e_over = 0.0;
+  bool unit_valid = false;
+  int s = 0;
+  // detail-only copies
+  double d_mwp = 0.0, d_cwp = 0.0, d_bw = 0.0, d_tm = 0.0, d_tc = 0.0, d_ts = 0.0, d_pu = 0.0, d_ps = 0.0, d_pm = 0.0, d_psm = 0.0,
+         d_ci = 0.0, d_act = 0.0, d_warps = 0.0, d_bps = 0.0, d_eta = 0.0, d_waves = 0.0;
   if (live) {
     int64_t ks, k;
-    int j, s;
+    int j;
     if (a.n_units <= 0x7fffffffLL) {                   // 32-bit index arithmetic on the common sizes
       const uint32_t u32 = (uint32_t)unit, ks32 = u32 / (uint32_t)a.n_shapes, k32 = ks32 / (uint32_t)a.n_specs;
       j = (int)(u32 - ks32 * (uint32_t)a.n_shapes); s = (int)(ks32 - k32 * (uint32_t)a.n_specs);
@@ -166,7 +174,7 @@ predict_grid_kernel(GridArgs a) {
       fits = fits && reg_limit >= 1.0;
     }
     if (ovr) bps = f[FFB_F_OVR_BPS];
-    const bool unit_valid = (a.strict || ovr) ? shape_ok : (shape_ok && fits);
+    unit_valid = (a.strict || ovr) ? shape_ok : (shape_ok && fits);
     const double eta = ovr ? f[FFB_F_OVR_ETA]
                            : py_min(1.0, (double)bx / 32.0) * f[FFB_F_ALIGNED];   // features.py:59
 
@@ -183,7 +191,7 @@ predict_grid_kernel(GridArgs a) {
     const double nc = kr[KS_N_COMP] * waves;
     const double t_comp = (nc > 0.0) ? nc / kr[KS_DENOM_COMP] : 0.0;
     const double t_sync = (f[FFB_F_N_SYNC] * waves) * sp[FFB_S_T_BARRIER];
-    const double t_exec = ((sp[FFB_S_W_MEM] * t_mem + sp[FFB_S_W_COMP] * t_comp) +
+    t_exec = ((sp[FFB_S_W_MEM] * t_mem + sp[FFB_S_W_COMP] * t_comp) +
                            sp[FFB_S_W_SYNC] * t_sync) + sp[FFB_S_T_BASE];
 
     // ---- power, cap-independent part (power_model.py:124-150) ----
@@ -205,72 +213,97 @@ predict_grid_kernel(GridArgs a) {
     }
     const double p_mem = sp[FFB_S_P_MEM_BASE] * (1.0 + sp[FFB_S_LAMBDA] * (1.0 - eta));
     const double p_sm = kr[KS_P_SM];
-    double p_pre = ((p_units + p_shape) + p_mem) + p_sm;
+    p_pre = ((p_units + p_shape) + p_mem) + p_sm;
     const double t_seen = (ovr && f[FFB_F_OVR_TEXEC] == f[FFB_F_OVR_TEXEC]) ? f[FFB_F_OVR_TEXEC] : t_exec;
     if (t_seen < sp[FFB_S_TAU_SHORT]) p_pre = p_pre * sp[FFB_S_TRANSIENT_R];      // power_model.py:93-95
-    const double p_static = sp[FFB_S_P_STATIC];
-    const double e_over = sp[FFB_S_E_OVERHEAD];
+    p_static = sp[FFB_S_P_STATIC];
+    e_over = sp[FFB_S_E_OVERHEAD];
+    if (kDetail) {
+      d_mwp = mwp; d_cwp = kr[KS_CWP]; d_bw = bw_eff; d_tm = t_mem; d_tc = t_comp; d_ts = t_sync; d_pu = p_units; d_ps = p_shape;
+      d_pm = p_mem; d_psm = p_sm; d_ci = ci; d_act = kr[KS_ACTIVE]; d_warps = (double)warps; d_bps = bps; d_eta = eta; d_waves = waves;
+    }
 
     if (!kLean) {
       if (a.occ) a.occ[unit] = bps;
       if (err && a.status) atomicOr(a.status, err);
     }
 
-    // ---- cap axis (power_model.py:152-158, explorer.py:107) ----
-    const double2* ct = reinterpret_cast<const double2*>(a.tb.cap_tab + (size_t)s * C * 4);
-    const bool any_cap = kLean ? false : (a.strict != 0);
-    for (int c = 0; c < C; ++c) {
-      const double2 sc_cap = ct[2 * c], room_ok = ct[2 * c + 1];
-      double p_dyn = p_pre * sc_cap.x;
-      const bool limited = p_dyn + p_static > sc_cap.y;
-      if (limited) p_dyn = room_ok.x;                       // max(0.0, cap - p_static), tabulated
-      const double e_pred = t_exec * (p_dyn + p_static) + e_over;
-      const bool ok = unit_valid && (any_cap || room_ok.y != 0.0);
-      const size_t o = (size_t)threadIdx.x * C + c;
-      s_t[o] = ok ? t_exec : INFINITY;
-      s_e[o] = ok ? e_pred : INFINITY;
-      if (!kLean) {
-        if (a.pdyn) s_p[o] = p_dyn;
-        if (a.flags) s_f[o] = (uint8_t)((ok ? FFB_PT_VALID : 0) | (limited ? FFB_PT_CAP_LIMITED : 0));
-      }
-      if (kDetail) {
-        double* d = a.detail + ((size_t)unit * C + c) * FFB_DETAIL_WIDTH;
-        d[FFB_D_MWP] = mwp; d[FFB_D_CWP] = kr[KS_CWP]; d[FFB_D_BW_EFF] = bw_eff;
-        d[FFB_D_T_MEM] = t_mem; d[FFB_D_T_COMP] = t_comp; d[FFB_D_T_SYNC] = t_sync;
-        d[FFB_D_T_EXEC] = t_exec; d[FFB_D_P_UNITS] = p_units; d[FFB_D_P_SHAPE] = p_shape;
-        d[FFB_D_P_MEM] = p_mem; d[FFB_D_P_SM] = p_sm; d[FFB_D_P_DYN] = p_dyn;
-        d[FFB_D_F_ADJ] = a.tb.cap_fadj[(size_t)s * C + c]; d[FFB_D_CI] = ci;
-        d[FFB_D_ACTIVE_SMS] = kr[KS_ACTIVE]; d[FFB_D_CAP_LIMITED] = limited ? 1.0 : 0.0;
-        d[FFB_D_E_PRED] = e_pred; d[FFB_D_WARPS] = (double)warps; d[FFB_D_BLOCKS_PER_SM] = bps;
-        d[FFB_D_ETA] = eta; d[FFB_D_WAVES] = waves;
-      }
-    }
   }
-  __syncthreads();
 
-  // ---- coalesced write-out of the [units, C] tile ----
+  // ---- cap axis (power_model.py:152-158, explorer.py:107), CT caps per pass ----
   const int64_t rem = a.n_units - unit0;
   const int n_live = rem < kUnitsPerCta ? (int)rem : kUnitsPerCta;
-  const size_t base = (size_t)unit0 * C;
-  const int total = n_live * C;
-  if (kLean && (base & 1) == 0) {
-    // 16-byte stores: the tile starts on an even element, so (t + base) is 16-byte aligned
-    const int pairs = total >> 1;
-    double2* gt = reinterpret_cast<double2*>(a.t + base);
-    double2* ge = reinterpret_cast<double2*>(a.e + base);
-    const double2* st2 = reinterpret_cast<const double2*>(s_t);
-    const double2* se2 = reinterpret_cast<const double2*>(s_e);
-    for (int i = threadIdx.x; i < pairs; i += kUnitsPerCta) { gt[i] = st2[i]; ge[i] = se2[i]; }
-    if ((total & 1) && threadIdx.x == 0) { a.t[base + total - 1] = s_t[total - 1]; a.e[base + total - 1] = s_e[total - 1]; }
-  } else {
-    for (int i = threadIdx.x; i < total; i += kUnitsPerCta) {
-      if (a.t) a.t[base + i] = s_t[i];
-      if (a.e) a.e[base + i] = s_e[i];
-      if (!kLean) {
-        if (a.pdyn) a.pdyn[base + i] = s_p[i];
-        if (a.flags) a.flags[base + i] = s_f[i];
+  for (int c0 = 0; c0 < C; c0 += CT) {
+    const int ct = C - c0 < CT ? C - c0 : CT;
+    if (live) {
+      const double2* ct2 = reinterpret_cast<const double2*>(a.tb.cap_tab + ((size_t)s * C + c0) * 4);
+      const bool any_cap = kLean ? false : (a.strict != 0);
+      for (int c = 0; c < ct; ++c) {
+        const double2 sc_cap = ct2[2 * c], room_ok = ct2[2 * c + 1];
+        double p_dyn = p_pre * sc_cap.x;
+        const bool limited = p_dyn + p_static > sc_cap.y;
+        if (limited) p_dyn = room_ok.x;                       // max(0.0, cap - p_static), tabulated
+        const double e_pred = t_exec * (p_dyn + p_static) + e_over;
+        const bool ok = unit_valid && (any_cap || room_ok.y != 0.0);
+        const size_t o = (size_t)threadIdx.x * ct + c;
+        s_t[o] = ok ? t_exec : INFINITY;
+        s_e[o] = ok ? e_pred : INFINITY;
+        if (!kLean) {
+          if (a.pdyn) s_p[o] = p_dyn;
+          if (a.flags) s_f[o] = (uint8_t)((ok ? FFB_PT_VALID : 0) | (limited ? FFB_PT_CAP_LIMITED : 0));
+        }
+        if (kDetail) {
+          double* d = a.detail + ((size_t)unit * C + c0 + c) * FFB_DETAIL_WIDTH;
+          d[FFB_D_MWP] = d_mwp; d[FFB_D_CWP] = d_cwp; d[FFB_D_BW_EFF] = d_bw;
+          d[FFB_D_T_MEM] = d_tm; d[FFB_D_T_COMP] = d_tc; d[FFB_D_T_SYNC] = d_ts;
+          d[FFB_D_T_EXEC] = t_exec; d[FFB_D_P_UNITS] = d_pu; d[FFB_D_P_SHAPE] = d_ps;
+          d[FFB_D_P_MEM] = d_pm; d[FFB_D_P_SM] = d_psm; d[FFB_D_P_DYN] = p_dyn;
+          d[FFB_D_F_ADJ] = a.tb.cap_fadj[(size_t)s * C + c0 + c]; d[FFB_D_CI] = d_ci;
+          d[FFB_D_ACTIVE_SMS] = d_act; d[FFB_D_CAP_LIMITED] = limited ? 1.0 : 0.0;
+          d[FFB_D_E_PRED] = e_pred; d[FFB_D_WARPS] = d_warps; d[FFB_D_BLOCKS_PER_SM] = d_bps;
+          d[FFB_D_ETA] = d_eta; d[FFB_D_WAVES] = d_waves;
+        }
       }
     }
+    __syncthreads();
+
+    // ---- coalesced write-out of the [units, ct] tile ----
+    const int total = n_live * ct;
+    if (ct == C) {
+      const size_t base = (size_t)unit0 * C;
+      if (kLean && (base & 1) == 0) {
+        // 16-byte stores: the tile starts on an even element, so (t + base) is 16-byte aligned
+        const int pairs = total >> 1;
+        double2* gt = reinterpret_cast<double2*>(a.t + base);
+        double2* ge = reinterpret_cast<double2*>(a.e + base);
+        const double2* st2 = reinterpret_cast<const double2*>(s_t);
+        const double2* se2 = reinterpret_cast<const double2*>(s_e);
+        for (int i = threadIdx.x; i < pairs; i += kUnitsPerCta) { gt[i] = st2[i]; ge[i] = se2[i]; }
+        if ((total & 1) && threadIdx.x == 0) { a.t[base + total - 1] = s_t[total - 1]; a.e[base + total - 1] = s_e[total - 1]; }
+      } else {
+        for (int i = threadIdx.x; i < total; i += kUnitsPerCta) {
+          if (a.t) a.t[base + i] = s_t[i];
+          if (a.e) a.e[base + i] = s_e[i];
+          if (!kLean) {
+            if (a.pdyn) a.pdyn[base + i] = s_p[i];
+            if (a.flags) a.flags[base + i] = s_f[i];
+          }
+        }
+      }
+    } else {
+      // cap axis in several passes: runs of ct values per unit
+      for (int i = threadIdx.x; i < total; i += kUnitsPerCta) {
+        const int u = i / ct, c = i - u * ct;
+        const size_t o = (size_t)(unit0 + u) * C + c0 + c;
+        if (a.t) a.t[o] = s_t[i];
+        if (a.e) a.e[o] = s_e[i];
+        if (!kLean) {
+          if (a.pdyn) a.pdyn[o] = s_p[i];
+          if (a.flags) a.flags[o] = s_f[i];
+        }
+      }
+    }
+    if (c0 + CT < C) __syncthreads();
   }
 }
 
@@ -416,9 +449,13 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   a.n_units = K * S * J; a.n_specs = (int)S; a.n_shapes = (int)J; a.n_caps = (int)C;
   a.t = g->d_t; a.e = g->d_e; a.pdyn = g->d_pdyn; a.flags = g->d_flags; a.occ = g->d_occ;
   a.detail = g->d_detail; a.status = g->d_status; a.strict = g->strict;
-  const size_t smem = (size_t)kUnitsPerCta * C * (2 * sizeof(double) + (g->d_pdyn ? sizeof(double) : 0) + 1);
-  if (smem > 200 * 1024)
-    return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_predict_grid: %lld caps exceed the shared-memory tile", (long long)C);
+  // the [units, caps] staging tile holds the whole cap axis when it fits 200 KB (47 caps, 32 with p_dyn);
+  // longer cap lists are walked in passes of that many caps
+  const size_t per_cap = (size_t)kUnitsPerCta * (2 * sizeof(double) + (g->d_pdyn ? sizeof(double) : 0) + 1);
+  int64_t cap_tile = (int64_t)((200 * 1024) / per_cap);
+  if (cap_tile > C) cap_tile = C;
+  a.cap_tile = (int)cap_tile;
+  const size_t smem = per_cap * (size_t)cap_tile;
   const int64_t n_cta = (a.n_units + kUnitsPerCta - 1) / kUnitsPerCta;
   if (n_cta > 0x7fffffffLL) return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_predict_grid: grid too large for one launch");
   const bool lean = !g->d_detail && !g->d_pdyn && !g->d_flags && !g->d_occ && !g->strict && !g->d_status && g->d_t && g->d_e;

@@ -102,6 +102,27 @@ def score_grid(feat: torch.Tensor, res: torch.Tensor, spec: np.ndarray, shape: n
     return r
 
 
+def score_grid_sweep(feat: torch.Tensor, res_axis: torch.Tensor, spec: np.ndarray, shape: np.ndarray, cap: np.ndarray,
+                     **kw) -> GridResult:
+    """Workload sweep in ONE launch: every kernel is scored under R resource rows
+    (e.g. one per sequence length, launch.py:44-82).  ``res_axis`` is int64 [R, 2] (the same rows for
+    every kernel) or [K, R, 2]; the kernel rows are replicated R times on the device and the grid
+    kernel runs once over K*R rows.  Outputs gain an axis: t / e / ... [K, R, S, J, C], occ [K, R, S, J]."""
+    K = feat.shape[0]
+    if res_axis.dim() == 2:
+        res_axis = res_axis.unsqueeze(0).expand(K, -1, -1)
+    assert res_axis.dtype == torch.int64 and res_axis.shape[0] == K and res_axis.shape[2] == 2
+    R = res_axis.shape[1]
+    feat_r = feat.repeat_interleave(R, dim=0).contiguous()
+    res_r = res_axis.reshape(K * R, 2).contiguous()
+    r = score_grid(feat_r, res_r, spec, shape, cap, **kw)
+    for name in ("t", "e", "pdyn", "flags", "occ", "detail"):
+        v = getattr(r, name)
+        if v is not None:
+            setattr(r, name, v.view(K, R, *v.shape[1:]))
+    return r
+
+
 def enumerate_shapes(spec_row: np.ndarray, shared_dyn: int, dims, rt: native.Runtime | None = None) -> np.ndarray:
     """Valid (bx, by) pairs in canonical (threads, bx, by) order — explorer.py:76-88,93."""
     lib = (rt or native.get_runtime()).lib

@@ -76,14 +76,39 @@ def declared_symbols() -> tuple[str, ...]:
     return tuple(_SIGNATURES)
 
 
+class _LockedLib:
+    """The context is not thread-safe by itself (include/ffb.h): its host staging buffer, table
+    shadow and scratch reservations are per context.  Every ffb_* call made through a Runtime
+    therefore holds the runtime's lock, so Python threads sharing the per-device runtime
+    (the reference's ``evaluate_configs(jobs>1)`` is reentrant, explorer.py:177-179) cannot
+    interleave inside a call.  Ordering on the device is the stream's; a context serves one
+    stream at a time unless the caller orders the streams itself (corpus.StreamedAnalysis does)."""
+
+    def __init__(self, lib: C.CDLL, lock: threading.RLock):
+        self._lib, self._lock = lib, lock
+
+    def __getattr__(self, name):
+        fn = getattr(self._lib, name)
+        lock = self._lock
+
+        def call(*args):
+            with lock:
+                return fn(*args)
+        call.__name__ = name
+        setattr(self, name, call)
+        return call
+
+
 class Runtime:
     """One libffb context on one device plus tensor helpers."""
 
     def __init__(self, lib: C.CDLL, device: torch.device, device_index: int = 0):
-        self.lib = lib
+        self.lock = threading.RLock()
+        self.raw_lib = lib
+        self.lib = _LockedLib(lib, self.lock)
         self.device = device
         handle = _vp()
-        rc = lib.ffb_create(device_index, C.byref(handle))
+        rc = self.lib.ffb_create(device_index, C.byref(handle))
         if rc != 0 or not handle.value:
             raise NativeLibraryMissing(f"ffb_create failed on device {device_index} (status {rc})")
         self.ctx = handle

@@ -229,3 +229,45 @@ def pack_spec(arch: ArchitectureSpec, profile: CalibrationProfile, regs_per_sm: 
     assert len(row) == len(SPEC_COLUMNS)
     row = [float(x) for x in row]
     return row + [0.0] * (SPEC_WIDTH - len(row))
+
+
+# ---------------------------------------------------------------- spec directories
+
+SPEC_DIR = Path(__file__).resolve().parent / "spec_files"
+
+
+def load_regs_per_sm(path) -> int:
+    """Optional ``extensions.regs_per_sm`` of a profile file (the reference's loader ignores
+    unknown keys, calibration.py:358-478; 0 = no register limit = reference behaviour)."""
+    obj = _read_json(path)
+    ext = obj.get("extensions", {}) if isinstance(obj, dict) else {}
+    if not isinstance(ext, dict):
+        raise SchemaViolation(f"{path}.extensions: must be an object")
+    v = ext.get("regs_per_sm", 0)
+    if not _is_num(v) or v < 0 or v != int(v):
+        raise SchemaViolation(f"{path}.extensions.regs_per_sm: must be a non-negative integer")
+    return int(v)
+
+
+def load_profiles(directory=None, *, with_register_limit: bool = False):
+    """Every ``*.json`` profile of a directory (default: the authored spec files shipped with the
+    package), sorted by file name, as the packed SoA the grid kernel consumes.
+
+    Returns ``(names, pairs, rows)``: architecture names, the ``(ArchitectureSpec,
+    CalibrationProfile)`` pairs exactly as ``load_profile`` returns them, and a float64
+    ``[S, SPEC_WIDTH]`` array (``pack_spec`` per file).  ``with_register_limit`` also packs the
+    files' ``extensions.regs_per_sm`` (extension, off by default = reference behaviour)."""
+    import numpy as np
+    directory = Path(directory) if directory is not None else SPEC_DIR
+    files = sorted(p for p in directory.glob("*.json"))
+    if not files:
+        raise SchemaViolation(f"{directory}: no *.json profile found")
+    names, pairs, rows = [], [], []
+    for f in files:
+        arch, prof = load_profile(f)
+        names.append(arch.name)
+        pairs.append((arch, prof))
+        rows.append(pack_spec(arch, prof, load_regs_per_sm(f) if with_register_limit else 0))
+    if len(set(names)) != len(names):
+        raise SchemaViolation(f"{directory}: duplicate architecture names {sorted(names)}")
+    return names, pairs, np.ascontiguousarray(np.asarray(rows, dtype=np.float64).reshape(len(rows), SPEC_WIDTH))
