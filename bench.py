@@ -45,6 +45,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunk-mb", type=int, default=384, help="chunk size of the overlapped host->device pipeline of the e2e leg")
     ap.add_argument("--lex-flags", type=int, default=0, help="FFB_LEX_* bits for A/B runs (2 = no lock-step CTAs)")
+    ap.add_argument("--unfused", action="store_true", help="score + front as two kernels with the [K,S,J,C] grid in HBM "
+                    "(ffb_predict_grid -> ffb_skyline_groups) instead of the fused ffb_explore_groups")
     return ap.parse_args()
 
 
@@ -196,7 +198,9 @@ def main():
     front_total = int(fn0.sum().item())
     assert int(fn0.min().item()) >= 1, "a kernel produced an empty front"
     fn0_host = fn0.cpu().numpy().astype(np.int64)
-    del fn0
+    del fn0, r0
+    if not args.unfused:
+        bufs = None            # the fused step never materialises the grid; the sizing pass above doubles as its cross-check
     torch.cuda.empty_cache()
     cap_front = front_total + 1024
     front_bufs = (torch.empty((cap_front,), dtype=torch.int32, device=dev), torch.empty((K,), dtype=torch.int32, device=dev),
@@ -230,11 +234,15 @@ def main():
         fn, tp, fo = front_bufs[1], front_bufs[2], front_bufs[3]
 
         def on_chunk(c, s0, s1):
-            r = engine.score_grid(lex_state.feat[s0:s1], res[s0:s1], sp, shp, CAPS, want=("t", "e"),
-                                  out={"t": bufs["t"][s0:s1], "e": bufs["e"][s0:s1]}, check=False, rt=rt)
             lo, hi = e2e["regions"][c]
-            engine.skyline_groups(r.e.view(-1), r.t.view(-1), s1 - s0, G, tie=d_tie, rho=RHO, compact=True, cap_front=hi - lo,
-                                  out=(e2e["front"][lo:hi], fn[s0:s1], tp[s0:s1], fo[s0:s1]), check=False, rt=rt)
+            if args.unfused:
+                r = engine.score_grid(lex_state.feat[s0:s1], res[s0:s1], sp, shp, CAPS, want=("t", "e"),
+                                      out={"t": bufs["t"][s0:s1], "e": bufs["e"][s0:s1]}, check=False, rt=rt)
+                engine.skyline_groups(r.e.view(-1), r.t.view(-1), s1 - s0, G, tie=d_tie, rho=RHO, compact=True, cap_front=hi - lo,
+                                      out=(e2e["front"][lo:hi], fn[s0:s1], tp[s0:s1], fo[s0:s1]), check=False, rt=rt)
+            else:
+                engine.explore_groups(lex_state.feat[s0:s1], res[s0:s1], sp, shp, CAPS, rho=RHO, compact=True, cap_front=hi - lo,
+                                      out=(e2e["front"][lo:hi], fn[s0:s1], tp[s0:s1], fo[s0:s1]), check=False, rt=rt)
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 e2e["h_front"][lo:hi].copy_(e2e["front"][lo:hi], non_blocking=True)
@@ -261,11 +269,17 @@ def main():
             marks[4].record()
         if timed:
             marks[1].record()
-        r = engine.score_grid(feat, res, sp, shp, CAPS, want=("t", "e"), out=bufs, check=False, rt=rt)
-        if timed:
-            marks[2].record()
-        fi, fn, tp, fo = engine.skyline_groups(r.e.view(-1), r.t.view(-1), K, G, tie=d_tie, rho=RHO, compact=True,
-                                               cap_front=cap_front, out=front_bufs, check=False, rt=rt)
+        if args.unfused:
+            r = engine.score_grid(feat, res, sp, shp, CAPS, want=("t", "e"), out=bufs, check=False, rt=rt)
+            if timed:
+                marks[2].record()
+            fi, fn, tp, fo = engine.skyline_groups(r.e.view(-1), r.t.view(-1), K, G, tie=d_tie, rho=RHO, compact=True,
+                                                   cap_front=cap_front, out=front_bufs, check=False, rt=rt)
+        else:
+            if timed:
+                marks[2].record()                                 # fused: score and front are one kernel, timed as "front"
+            fi, fn, tp, fo = engine.explore_groups(feat, res, sp, shp, CAPS, rho=RHO, compact=True, cap_front=cap_front,
+                                                   out=front_bufs, check=False, rt=rt)
         if timed:
             marks[3].record()
         if not resident:
@@ -350,6 +364,7 @@ def main():
     _, (fi, fn) = step(True, False)
     torch.cuda.synchronize()
     assert int(fn.min()) >= 1 and int(fn.sum()) == front_total, "fronts changed between steps"
+    assert np.array_equal(fn.cpu().numpy().astype(np.int64), fn0_host), "front sizes differ from the two-call sizing pass"
     if e2e_host is not None:
         hn, ho, hf = e2e_host
         assert torch.equal(hn, fn.cpu()), "streamed e2e leg: front sizes differ from the resident pass"
@@ -374,12 +389,23 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    kernels = {
-        "score": {"kernel": "predict_grid_kernel", "ncu_name": "predict_grid_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["score"],
-                  "bytes_per_unit": "16 B written per grid point (t_exec, e_pred f64)"},
-        "front": {"kernel": "skyline_group_kernel", "ncu_name": "skyline_group_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["front"],
-                  "bytes_per_unit": "16 B read per candidate (e, t f64)"},
-    }
+    if args.unfused:
+        kernels = {
+            "score": {"kernel": "predict_grid_kernel", "ncu_name": "predict_grid_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["score"],
+                      "bytes_per_unit": "16 B written per grid point (t_exec, e_pred f64)"},
+            "front": {"kernel": "skyline_group_kernel", "ncu_name": "skyline_group_kernel", "bytes": 16.0 * points_rank, "ms": phase_ms["front"],
+                      "bytes_per_unit": "16 B read per candidate (e, t f64)"},
+        }
+    else:
+        # fused K2+K3+K4: the 16 B per point of the two-call route never reach HBM; what the kernel must move is one
+        # feature row + resource row per kernel in and 4 B per front member (+ 20 B per group) out
+        kernels = {
+            "front": {"kernel": "explore_groups_kernel (K2+K3+K4 fused)", "ncu_name": "explore_groups_kernel",
+                      "bytes": float(K * (18 * 8 + 16) + front_total * 4 + K * 20), "ms": phase_ms["front"],
+                      "bytes_per_unit": "160 B read per kernel + 4 B written per front member; compute-bound by design "
+                                        "(the grid stays in shared memory), see points_per_s",
+                      "points_per_s": points_rank / (phase_ms["front"] / 1e3) if phase_ms["front"] > 0 else None},
+        }
     if corpus is not None:
         kernels["lex"] = {"kernel": "lex_fast_kernel<records>", "ncu_name": "lex_fast_kernel", "bytes": float(lex_bytes_rank), "ms": phase_ms["lex"],
                           "bytes_per_unit": "1 B read per PTX byte (+ ~2 B of records written per byte)"}

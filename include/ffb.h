@@ -157,6 +157,37 @@ int32_t ffb_skyline_groups(FfbContext* ctx, const double* d_e, const double* d_t
                            double* d_tpeak, int64_t cap_front, int64_t* d_front_off,
                            uint32_t* d_status, void* stream);
 
+/* ---- K2 + K3 + K4 fused: fronts only ----------------------------------------------------
+ * Stands in for pareto_explore (explorer.py:186-212): generate_valid_configs (:59-94, as the
+ * validity mask) -> evaluate_configs (:161-183) -> throughput floor (:209-210) -> pareto_front
+ * (:122-140), for every (kernel k, spec s) group at once; group g = k * n_specs + s holds the
+ * n_shapes * n_caps candidates of that kernel on that spec, candidate index j * n_caps + c.
+ * Same inputs as ffb_predict_grid, same outputs as ffb_skyline_groups with
+ * tie = rank of (block_x, block_y, block_z, regs) * n_caps + rank of the cap value - but the
+ * [K,S,J,C] grid never exists in HBM: one CTA evaluates a group into shared memory and ranks it
+ * there.  Results are identical to ffb_predict_grid + ffb_skyline_groups (tests compare them).
+ * d_front_e / d_front_t (optional) receive the (e_pred, t_exec) of every front member, parallel
+ * to d_front_idx.  Capacity: a group (n_shapes * n_caps candidates) must fit one CTA's shared
+ * memory, at most 32767 candidates (FFB_E_CAPACITY: use the two-call route). */
+typedef struct {
+  int64_t n_kernels, n_specs, n_shapes, n_caps;
+  const double*  d_feat;    /* [K, FFB_FEAT_WIDTH]                                         */
+  const int64_t* d_res;     /* [K, 2] {dynamic shared bytes, total blocks}                 */
+  const double*  h_spec;    /* [S, FFB_SPEC_WIDTH]                                         */
+  const int32_t* h_shape;   /* [J, 4] {block_x, block_y, block_z, regs_per_thread}         */
+  const double*  h_cap;     /* [C] watts                                                   */
+  double rho;               /* throughput floor, <= 0 disables it                          */
+  uint32_t* d_front_idx;    /* dense [K*S, cap_front] or compact [cap_front] (with d_front_off) */
+  uint32_t* d_front_n;      /* [K*S]                                                       */
+  double*   d_tpeak;        /* [K*S] or NULL                                               */
+  int64_t   cap_front;
+  int64_t*  d_front_off;    /* [K*S] or NULL (dense)                                       */
+  double*   d_front_e;      /* optional, laid out like d_front_idx                         */
+  double*   d_front_t;      /* optional                                                    */
+  uint32_t* d_status;       /* [1] OR-ed (1 << FFB_E_CAPACITY) when a front does not fit    */
+} FfbExploreDesc;
+int32_t ffb_explore_groups(FfbContext* ctx, const FfbExploreDesc* d, void* stream);
+
 /* One large candidate set (BASELINE config 5).  Streaming cull against a sentinel
  * staircase, exact pass on the survivors.  Output: global indices (or d_id values when
  * d_id != NULL) of the front in (e, t, id) order.  Syncs (returns the count).

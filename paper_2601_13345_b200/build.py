@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
           "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 # the fp64 model must not be contracted into FMAs: results are compared bit-for-bit
-PER_FILE = {"ffb_predict.cu": ["-fmad=false"]}
+PER_FILE = {"ffb_predict.cu": ["-fmad=false"], "ffb_explore.cu": ["-fmad=false"]}
 
 
 def _nvcc() -> str:

@@ -42,6 +42,9 @@ struct FfbContext {
   FfbBuf d_sky;        // skyline scratch
   FfbBuf d_lex;        // lexer scratch
   FfbBuf d_flow;       // dataflow scratch
+  FfbBuf d_explore;    // fused explore: tie ranks + counter
+  std::vector<uint16_t> explore_shadow;   // host copy of the tie-order table d_explore holds
+  void* explore_shadow_dev = nullptr;
   void* h_stage = nullptr;   // pinned staging for table uploads
   size_t h_stage_cap = 0;
   cudaEvent_t stage_free = nullptr;  // recorded after the last async copy out of h_stage

@@ -12,34 +12,16 @@
 // cap-independent chain once, then walks the cap axis (7 flops per cap).  Results are staged
 // in shared memory so that the [unit, cap] tile leaves the SM as fully coalesced 8-byte
 // stores: the kernel is an HBM write stream of 16 B per grid point.
-#include "ffb_common.cuh"
+#include "ffb_model.cuh"
 
-#include <math.h>
 #include <string.h>
 #include <algorithm>
+
+using namespace ffbm;
 
 namespace {
 
 constexpr int kUnitsPerCta = 256;
-constexpr int kKsWidth = 8;    // doubles per (kernel, spec) row
-constexpr int kSdWidth = 16;   // doubles per derived-spec row
-
-enum { KS_SHARED_LIMIT = 0, KS_DENOM_COMP, KS_CI, KS_P_SM, KS_N_COMP, KS_CWP, KS_ACTIVE, KS_ERR };
-enum { SD_MWP = 0, SD_FLOOR, SD_RATIO0 /* 5 entries */, SD_SKIPMASK = 7, SD_ERR = 8 };
-
-struct Tables {
-  const double* spec;      // [S, FFB_SPEC_WIDTH]
-  const double* sd;        // [S, kSdWidth]
-  const int32_t* shape;    // [J, 4]
-  const double* shape_log; // [J]
-  const double* cap;       // [C]
-  const double* cap_scale; // [S, C]  f_adj / f_base
-  const double* cap_fadj;  // [S, C]
-  const double* cap_ok;    // [S, C]  1.0 when p_cap_min <= cap <= p_tdp
-  const double* cap_tab;   // [S, C, 4] {scale, cap, max(0, cap - p_static), ok}: the cap axis in one 32-byte row
-  const double* psm;       // [S, psm_n]
-  int psm_n;
-};
 
 // ---- per (kernel, spec) hoisting --------------------------------------------------------
 __global__ void __launch_bounds__(256)
@@ -50,45 +32,8 @@ predict_prepare_kernel(const double* __restrict__ feat, const int64_t* __restric
   if (i >= n_kernels * n_specs) return;
   int64_t k = i / n_specs;
   int s = (int)(i - k * n_specs);
-  const double* f = feat + k * FFB_FEAT_WIDTH;
-  const double* sp = tb.spec + (size_t)s * FFB_SPEC_WIDTH;
-  const double* sd = tb.sd + (size_t)s * kSdWidth;
-  uint32_t err = 0;
-
-  const int64_t shared = (int64_t)f[FFB_F_STATIC_SHARED] + res[2 * k + 0];   // features.py:111
-  const int64_t total_blocks = res[2 * k + 1];
-  if (total_blocks <= 0) err |= 1u << FFB_E_EMPTY_GRID;                     // time_model.py:75
-  double shared_limit = INFINITY;
-  if (shared > 0) shared_limit = sp[FFB_S_MAX_SHARED] / (double)shared;       // features.py:113
-
-  // time_model.py:47-64 (_issue_window): FP32, INT, SFU weighted by exec/issue
-  double weighted = 0.0, total = 0.0;
-  for (int u = 0; u < 3; ++u) {
-    const double cnt = f[FFB_F_FP32 + u];
-    weighted = weighted + cnt * sd[SD_RATIO0 + u];
-    total = total + cnt;
-  }
-  const double window = (total <= 0.0) ? sd[SD_RATIO0 + 3] : weighted / total;
-  double cwp = 1.0;
-  if (window <= 0.0) err |= 1u << FFB_E_ZERO_COMPUTE;                       // time_model.py:42
-  else cwp = py_max(1.0, (sp[FFB_S_L_COAL] + window) / window);               // time_model.py:44
-  const bool ovr = f[FFB_F_OVR] != 0.0;
-  const double n_comp = ovr ? f[FFB_F_OVR_NCOMP]
-                            : (f[FFB_F_FP32] + f[FFB_F_INT]) + f[FFB_F_SFU];  // features.py:108
-  const double n_mem = f[FFB_F_N_MEM];
-  const double ci = (n_mem == 0.0) ? INFINITY : n_comp / n_mem;               // power_model.py:44-46
-  const int64_t sm = (int64_t)sp[FFB_S_SM_COUNT];
-  int64_t active = total_blocks < sm ? total_blocks : sm;                    // power_model.py:86
-  if (active < 0) active = 0;
-  double* o = kstab + i * kKsWidth;
-  o[KS_SHARED_LIMIT] = shared_limit;
-  o[KS_DENOM_COMP] = (cwp * sp[FFB_S_IPC]) * sp[FFB_S_F_BASE];                // time_model.py:116
-  o[KS_CI] = ci;
-  o[KS_P_SM] = tb.psm[(size_t)s * tb.psm_n + active];                         // power_model.py:74-76
-  o[KS_N_COMP] = n_comp;
-  o[KS_CWP] = cwp;
-  o[KS_ACTIVE] = (double)active;
-  o[KS_ERR] = (double)err;
+  const uint32_t err = eval_kernel_spec(feat + k * FFB_FEAT_WIDTH, res[2 * k + 0], res[2 * k + 1], tb.spec + (size_t)s * FFB_SPEC_WIDTH,
+                                        tb.sd + (size_t)s * kSdWidth, tb.psm + (size_t)s * tb.psm_n, kstab + i * kKsWidth);
   if (err && status) atomicOr(status, err);
 }
 
@@ -144,83 +89,16 @@ predict_grid_kernel(GridArgs a) {
       ks = unit / a.n_shapes; j = (int)(unit - ks * a.n_shapes);
       k = ks / a.n_specs; s = (int)(ks - k * a.n_specs);
     }
-    const double* f = a.feat + k * FFB_FEAT_WIDTH;
-    const double* sp = a.tb.spec + (size_t)s * FFB_SPEC_WIDTH;
-    const double* sd = a.tb.sd + (size_t)s * kSdWidth;
-    const double* kr = a.kstab + ks * kKsWidth;
-    const int32_t* sh = a.tb.shape + 4 * j;
-    const int64_t bx = sh[0], by = sh[1], bz = sh[2], regs = sh[3];
-    uint32_t err = (uint32_t)kr[KS_ERR] | (uint32_t)sd[SD_ERR];
-
-    // ---- K2: integer occupancy / validity (explorer.py:76-88, features.py:96-114) ----
-    const int64_t threads = bx * by * bz;
-    const int64_t max_threads = (int64_t)sp[FFB_S_MAX_THREADS];
-    const int64_t max_warps = (int64_t)sp[FFB_S_MAX_WARPS];
-    const int64_t shared_dyn = a.res[2 * k + 0];
-    const int64_t total_blocks = a.res[2 * k + 1];
-    const bool ovr = f[FFB_F_OVR] != 0.0;
-    const bool shape_ok = ovr || (threads >= 32 && threads <= max_threads && (threads % 32) == 0);
-    if (!shape_ok) err |= (a.strict ? 1u << FFB_E_INVALID_CONFIG : 0u);
-    const int64_t warps = ovr ? (int64_t)f[FFB_F_OVR_WARPS] : (shape_ok ? threads / 32 : 1);
-    bool fits = warps <= max_warps;                                   // max_warps/warps >= 1.0
-    if (shared_dyn > 0) fits = fits && shared_dyn <= (int64_t)sp[FFB_S_MAX_SHARED];
-    const double wf = (double)warps;
-    double bps = sp[FFB_S_MAX_WARPS] / wf;                            // features.py:112
-    bps = py_min(bps, kr[KS_SHARED_LIMIT]);                           // features.py:114
-    const double regs_per_sm = sp[FFB_S_REGS_PER_SM];
-    if (regs_per_sm > 0.0 && regs > 0) {                              // extension, see DESIGN.md
-      const double reg_limit = regs_per_sm / (double)(regs * threads);
-      bps = py_min(bps, reg_limit);
-      fits = fits && reg_limit >= 1.0;
-    }
-    if (ovr) bps = f[FFB_F_OVR_BPS];
-    unit_valid = (a.strict || ovr) ? shape_ok : (shape_ok && fits);
-    const double eta = ovr ? f[FFB_F_OVR_ETA]
-                           : py_min(1.0, (double)bx / 32.0) * f[FFB_F_ALIGNED];   // features.py:59
-
-    // ---- time (time_model.py:67-129) ----
-    const double resident = py_min(bps * wf, (double)max_warps);
-    const double lanes = (sp[FFB_S_SM_COUNT] * resident) * 32.0;
-    const double tthreads = (double)(total_blocks * warps) * 32.0;
-    const double waves = py_max(1.0, tthreads / lanes);
-    const double mwp = sd[SD_MWP];
-    const double bw_eff = sp[FFB_S_BW_MAX] * py_max(eta, sd[SD_FLOOR]);
-    const double mb = f[FFB_F_MEM_BYTES] * waves;
-    if (mb > 0.0 && bw_eff <= 0.0) err |= 1u << FFB_E_ZERO_BANDWIDTH;
-    const double t_mem = (mb > 0.0) ? mb / (mwp * bw_eff) : 0.0;
-    const double nc = kr[KS_N_COMP] * waves;
-    const double t_comp = (nc > 0.0) ? nc / kr[KS_DENOM_COMP] : 0.0;
-    const double t_sync = (f[FFB_F_N_SYNC] * waves) * sp[FFB_S_T_BARRIER];
-    t_exec = ((sp[FFB_S_W_MEM] * t_mem + sp[FFB_S_W_COMP] * t_comp) +
-                           sp[FFB_S_W_SYNC] * t_sync) + sp[FFB_S_T_BASE];
-
-    // ---- power, cap-independent part (power_model.py:124-150) ----
-    const double wps = py_min(wf * bps, (double)max_warps);
-    double p_units = 0.0;
-    const uint32_t skip = (uint32_t)sd[SD_SKIPMASK];
-#pragma unroll
-    for (int u = 0; u < 5; ++u) {
-      if (skip & (1u << u)) continue;
-      const double cnt = (u == 4) ? f[FFB_F_N_MEM] : f[FFB_F_FP32 + u];
-      const double rate = (cnt * wps) / sd[SD_RATIO0 + u];
-      p_units = p_units + sp[FFB_S_BETA0 + u] * rate;
-    }
-    const double ci = kr[KS_CI];
-    double p_shape = sp[FFB_S_P_BASE_SHAPE];
-    if (!isinf(ci)) {
-      const double penalty = (sp[FFB_S_KAPPA] * a.tb.shape_log[j]) / (1.0 + ci);
-      p_shape = sp[FFB_S_P_BASE_SHAPE] * (1.0 + penalty);
-    }
-    const double p_mem = sp[FFB_S_P_MEM_BASE] * (1.0 + sp[FFB_S_LAMBDA] * (1.0 - eta));
-    const double p_sm = kr[KS_P_SM];
-    p_pre = ((p_units + p_shape) + p_mem) + p_sm;
-    const double t_seen = (ovr && f[FFB_F_OVR_TEXEC] == f[FFB_F_OVR_TEXEC]) ? f[FFB_F_OVR_TEXEC] : t_exec;
-    if (t_seen < sp[FFB_S_TAU_SHORT]) p_pre = p_pre * sp[FFB_S_TRANSIENT_R];      // power_model.py:93-95
-    p_static = sp[FFB_S_P_STATIC];
-    e_over = sp[FFB_S_E_OVERHEAD];
+    Unit u;
+    eval_unit(a.feat + k * FFB_FEAT_WIDTH, a.tb.spec + (size_t)s * FFB_SPEC_WIDTH, a.tb.sd + (size_t)s * kSdWidth,
+              a.kstab + ks * kKsWidth, a.tb.shape + 4 * j, a.tb.shape_log[j], a.res[2 * k + 0], a.res[2 * k + 1], a.strict, u);
+    unit_valid = u.valid; t_exec = u.t_exec; p_pre = u.p_pre; p_static = u.p_static; e_over = u.e_over;
+    const uint32_t err = u.err;
+    const double bps = u.bps;
     if (kDetail) {
-      d_mwp = mwp; d_cwp = kr[KS_CWP]; d_bw = bw_eff; d_tm = t_mem; d_tc = t_comp; d_ts = t_sync; d_pu = p_units; d_ps = p_shape;
-      d_pm = p_mem; d_psm = p_sm; d_ci = ci; d_act = kr[KS_ACTIVE]; d_warps = (double)warps; d_bps = bps; d_eta = eta; d_waves = waves;
+      d_mwp = u.mwp; d_cwp = a.kstab[ks * kKsWidth + KS_CWP]; d_bw = u.bw_eff; d_tm = u.t_mem; d_tc = u.t_comp; d_ts = u.t_sync;
+      d_pu = u.p_units; d_ps = u.p_shape; d_pm = u.p_mem; d_psm = u.p_sm; d_ci = u.ci; d_act = a.kstab[ks * kKsWidth + KS_ACTIVE];
+      d_warps = (double)u.warps; d_bps = u.bps; d_eta = u.eta; d_waves = u.waves;
     }
 
     if (!kLean) {
@@ -240,10 +118,9 @@ predict_grid_kernel(GridArgs a) {
       const bool any_cap = kLean ? false : (a.strict != 0);
       for (int c = 0; c < ct; ++c) {
         const double2 sc_cap = ct2[2 * c], room_ok = ct2[2 * c + 1];
-        double p_dyn = p_pre * sc_cap.x;
-        const bool limited = p_dyn + p_static > sc_cap.y;
-        if (limited) p_dyn = room_ok.x;                       // max(0.0, cap - p_static), tabulated
-        const double e_pred = t_exec * (p_dyn + p_static) + e_over;
+        double p_dyn;
+        bool limited;
+        const double e_pred = eval_cap(t_exec, p_pre, p_static, e_over, sc_cap.x, sc_cap.y, room_ok.x, &p_dyn, &limited);
         const bool ok = unit_valid && (any_cap || room_ok.y != 0.0);
         const size_t o = (size_t)threadIdx.x * ct + c;
         s_t[o] = ok ? t_exec : INFINITY;
@@ -336,22 +213,13 @@ static int32_t validate_spec_row(FfbContext* ctx, const double* sp, int s, int s
   return FFB_OK;
 }
 
-extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void* stream_) {
-  if (!ctx || !g) return FFB_E_BAD_ARGUMENT;
-  cudaStream_t stream = (cudaStream_t)stream_;
-  const int64_t K = g->n_kernels, S = g->n_specs, J = g->n_shapes, C = g->n_caps;
-  if (K < 0 || S <= 0 || J < 0 || C <= 0 || S > (1 << 20) || J > (1 << 28) || C > 4096)
-    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_predict_grid: bad extents K=%lld S=%lld J=%lld C=%lld",
-                    (long long)K, (long long)S, (long long)J, (long long)C);
-  if (!g->d_feat || !g->d_res || !g->h_spec || !g->h_shape || !g->h_cap)
-    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_predict_grid: null input");
-  if (K == 0 || J == 0) return FFB_OK;
-  FFB_CUDA(ctx, cudaSetDevice(ctx->device));
-
+int32_t ffb_build_tables(FfbContext* ctx, const double* h_spec_in, const int32_t* h_shape_in, const double* h_cap_in,
+                         FfbTableDims dims, int strict, cudaStream_t stream, ffbm::Tables* tb_out, uint32_t* host_err_out) {
+  const int64_t S = dims.S, J = dims.J, C = dims.C;
   // ---- host tables (libm here, same as the reference's math.log / ** ) ----
   int psm_n = 1;
   for (int64_t s = 0; s < S; ++s) {
-    double sm = g->h_spec[s * FFB_SPEC_WIDTH + FFB_S_SM_COUNT];
+    double sm = h_spec_in[s * FFB_SPEC_WIDTH + FFB_S_SM_COUNT];
     if (!(sm >= 0.0) || sm > 1e6) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "spec %lld: sm_count out of range", (long long)s);
     if ((int)sm + 1 > psm_n) psm_n = (int)sm + 1;
   }
@@ -376,13 +244,13 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   double* h_ok = h_fadj + n_sc;
   double* h_psm = h_ok + n_sc;
   int32_t* h_shape = (int32_t*)(h_psm + n_psm);
-  memcpy(h_spec, g->h_spec, n_spec * sizeof(double));
-  memcpy(h_cap, g->h_cap, n_cap * sizeof(double));
-  memcpy(h_shape, g->h_shape, (size_t)J * 4 * sizeof(int32_t));
+  memcpy(h_spec, h_spec_in, n_spec * sizeof(double));
+  memcpy(h_cap, h_cap_in, n_cap * sizeof(double));
+  memcpy(h_shape, h_shape_in, (size_t)J * 4 * sizeof(int32_t));
   uint32_t host_err = 0;
   for (int64_t s = 0; s < S; ++s) {
     const double* sp = h_spec + s * FFB_SPEC_WIDTH;
-    validate_spec_row(ctx, sp, (int)s, g->strict, h_sd + s * kSdWidth);
+    validate_spec_row(ctx, sp, (int)s, strict, h_sd + s * kSdWidth);
     host_err |= (uint32_t)h_sd[s * kSdWidth + SD_ERR];
     const double tdp = sp[FFB_S_P_TDP], fb = sp[FFB_S_F_BASE];
     const double inv_k = 1.0 / (double)(int64_t)sp[FFB_S_DVFS_K];          // power_model.py:106
@@ -390,7 +258,7 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
       const double cap = h_cap[c];
       const bool in_range = (sp[FFB_S_P_CAP_MIN] <= cap) && (cap <= tdp);      // explorer.py:90
       const bool legal = cap > 0.0 && tdp > 0.0 && cap <= tdp;                 // power_model.py:100-105
-      if (g->strict && !legal) host_err |= 1u << FFB_E_CAP_ABOVE_TDP;
+      if (strict && !legal) host_err |= 1u << FFB_E_CAP_ABOVE_TDP;
       double fadj = legal ? fb * pow(cap / tdp, inv_k) : fb;
       h_fadj[s * C + c] = fadj;
       h_scale[s * C + c] = fadj / fb;                                          // power_model.py:153
@@ -433,6 +301,26 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   tb.psm = tb.cap_ok + n_sc;
   tb.shape = (const int32_t*)(tb.psm + n_psm);
   tb.psm_n = psm_n;
+  *tb_out = tb;
+  *host_err_out = host_err;
+  return FFB_OK;
+}
+
+extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void* stream_) {
+  if (!ctx || !g) return FFB_E_BAD_ARGUMENT;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t K = g->n_kernels, S = g->n_specs, J = g->n_shapes, C = g->n_caps;
+  if (K < 0 || S <= 0 || J < 0 || C <= 0 || S > (1 << 20) || J > (1 << 28) || C > 4096)
+    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_predict_grid: bad extents K=%lld S=%lld J=%lld C=%lld",
+                    (long long)K, (long long)S, (long long)J, (long long)C);
+  if (!g->d_feat || !g->d_res || !g->h_spec || !g->h_shape || !g->h_cap)
+    return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_predict_grid: null input");
+  if (K == 0 || J == 0) return FFB_OK;
+  FFB_CUDA(ctx, cudaSetDevice(ctx->device));
+  Tables tb;
+  uint32_t host_err = 0;
+  int32_t rc = ffb_build_tables(ctx, g->h_spec, g->h_shape, g->h_cap, FfbTableDims{S, J, C}, g->strict, stream, &tb, &host_err);
+  if (rc) return rc;
 
   rc = ffb_reserve(ctx, &ctx->d_kstab, (size_t)K * S * kKsWidth * sizeof(double));
   if (rc) return rc;

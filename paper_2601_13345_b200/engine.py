@@ -181,6 +181,50 @@ def skyline_groups(e: torch.Tensor, t: torch.Tensor, n_groups: int, group_size: 
     return front_idx, front_n, tpeak
 
 
+def explore_groups(feat: torch.Tensor, res: torch.Tensor, spec: np.ndarray, shape: np.ndarray, cap: np.ndarray, *,
+                   rho: float = 0.95, cap_front: int | None = None, compact: bool = False, want_values: bool = False,
+                   out: tuple | None = None, check: bool = True, rt: native.Runtime | None = None):
+    """K2 + K3 + K4 fused (ffb_explore_groups): the front of every (kernel, spec) group, grid never materialised.
+
+    Same result as ``score_grid`` followed by ``skyline_groups`` with the reference tie key; group
+    g = k * S + s, candidate index j * C + c.  Dense: (front_idx [K*S, cap_front], front_n, t_peak);
+    ``compact=True``: (front_idx [cap_front], front_n, t_peak, front_off).  ``want_values`` appends
+    (front_e, front_t) laid out like front_idx.  ``out`` = preallocated (front_idx, front_n, t_peak, front_off)."""
+    rt = rt or native.get_runtime()
+    K, S, J, Cn = feat.shape[0], spec.shape[0], shape.shape[0], cap.shape[0]
+    assert feat.dtype == torch.float64 and feat.shape[1] == native.FEAT_WIDTH and feat.is_contiguous()
+    assert res.dtype == torch.int64 and tuple(res.shape) == (K, 2) and res.is_contiguous()
+    spec = np.ascontiguousarray(spec, dtype=np.float64)
+    shape = np.ascontiguousarray(shape, dtype=np.int32)
+    cap = np.ascontiguousarray(cap, dtype=np.float64)
+    n_groups = K * S
+    cap_front = int(cap_front if cap_front is not None else J * Cn)
+    if out is not None:
+        front_idx, front_n, tpeak, front_off = out
+    else:
+        front_idx = rt.empty((cap_front,) if compact else (n_groups, cap_front), torch.int32)
+        front_n = rt.empty((n_groups,), torch.int32)
+        tpeak = rt.empty((n_groups,), torch.float64)
+        front_off = rt.empty((n_groups,), torch.int64) if compact else None
+    fe = rt.empty(tuple(front_idx.shape), torch.float64) if want_values else None
+    ft = rt.empty(tuple(front_idx.shape), torch.float64) if want_values else None
+    status = torch.zeros(1, dtype=torch.int32, device=rt.device) if check else None
+    d = native.ExploreDesc(
+        n_kernels=K, n_specs=S, n_shapes=J, n_caps=Cn, d_feat=native.ptr(feat), d_res=native.ptr(res),
+        h_spec=spec.ctypes.data, h_shape=shape.ctypes.data, h_cap=cap.ctypes.data, rho=float(rho),
+        d_front_idx=native.ptr(front_idx), d_front_n=native.ptr(front_n), d_tpeak=native.ptr(tpeak), cap_front=cap_front,
+        d_front_off=native.ptr(front_off), d_front_e=native.ptr(fe), d_front_t=native.ptr(ft), d_status=native.ptr(status))
+    rc = rt.lib.ffb_explore_groups(rt.ctx, C.byref(d), rt.stream())
+    rt.check(rc, "ffb_explore_groups")
+    if check:
+        st = int(status.item()) & 0xFFFFFFFF
+        for code in range(1, 32):
+            if st & (1 << code):
+                raise_for_status(code, "explore: front buffer too small")
+    res_t = (front_idx, front_n, tpeak, front_off) if compact else (front_idx, front_n, tpeak)
+    return res_t + ((fe, ft) if want_values else ())
+
+
 def skyline(e: torch.Tensor, t: torch.Tensor, *, ids: torch.Tensor | None = None, rho: float = 0.0,
             cap_front: int = 1 << 16, rt: native.Runtime | None = None, occ: torch.Tensor | None = None):
     """K4 on one large candidate set.  Returns (ids, e, t, t_peak) of the front in (e, t, id) order."""

@@ -42,6 +42,15 @@ class GridDesc(C.Structure):
     ]
 
 
+class ExploreDesc(C.Structure):
+    _fields_ = [
+        ("n_kernels", _i64), ("n_specs", _i64), ("n_shapes", _i64), ("n_caps", _i64),
+        ("d_feat", _vp), ("d_res", _vp), ("h_spec", _vp), ("h_shape", _vp), ("h_cap", _vp),
+        ("rho", _f64), ("d_front_idx", _vp), ("d_front_n", _vp), ("d_tpeak", _vp), ("cap_front", _i64),
+        ("d_front_off", _vp), ("d_front_e", _vp), ("d_front_t", _vp), ("d_status", _vp),
+    ]
+
+
 _SIGNATURES = {
     "ffb_abi_version": (_i32, []),
     "ffb_create": (_i32, [_i32, C.POINTER(_vp)]),
@@ -49,6 +58,7 @@ _SIGNATURES = {
     "ffb_last_error": (C.c_char_p, [_vp]),
     "ffb_launch_count": (_i64, [_vp]),
     "ffb_predict_grid": (_i32, [_vp, C.POINTER(GridDesc), _vp]),
+    "ffb_explore_groups": (_i32, [_vp, C.POINTER(ExploreDesc), _vp]),
     "ffb_enumerate_shapes": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_i64)]),
     "ffb_skyline_groups": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "ffb_skyline_groups3": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),

@@ -119,6 +119,17 @@ inline unsigned __ballot_sync(unsigned, int pred) {
   pthread_barrier_wait(&w->bar);
   return m;
 }
+template <typename T> inline unsigned __match_any_sync(unsigned, T v) {
+  simt::WarpBox* w = simt::t_warp;
+  unsigned long long raw = 0;
+  memcpy(&raw, &v, sizeof(T));
+  w->slot[simt_lane()] = raw;
+  pthread_barrier_wait(&w->bar);
+  unsigned m = 0;
+  for (int i = 0; i < 32; ++i) m |= (unsigned)(w->slot[i] == raw) << i;
+  pthread_barrier_wait(&w->bar);
+  return m;
+}
 inline int __any_sync(unsigned m, int p) { return __ballot_sync(m, p) != 0; }
 inline int __all_sync(unsigned m, int p) { return __ballot_sync(m, p) == 0xffffffffu; }
 
@@ -151,6 +162,7 @@ template <typename T> inline T __ldg(const T* p) { return *p; }
 inline double __dadd_rn(double a, double b) { return a + b; }
 inline double __dmul_rn(double a, double b) { return a * b; }
 inline double __ddiv_rn(double a, double b) { return a / b; }
+inline unsigned __umulhi(unsigned a, unsigned b) { return (unsigned)(((unsigned long long)a * b) >> 32); }
 inline unsigned long long __umul64hi(unsigned long long a, unsigned long long b) {
   return (unsigned long long)(((unsigned __int128)a * b) >> 64);
 }
