@@ -37,6 +37,15 @@
 
 namespace {
 
+#ifdef FFB_SIMT_EMUL
+#define FFB_PREFETCH_L2(p) ((void)(p))
+#else
+#define FFB_PREFETCH_L2(p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p))
+#endif
+#ifndef FFB_LEX_PREFETCH
+#define FFB_LEX_PREFETCH 1
+#endif
+constexpr bool kPrefetch = FFB_LEX_PREFETCH != 0;
 constexpr int kFWarps = 4;
 constexpr int kFTile = 4096;
 constexpr int kFPad = 64;
@@ -48,7 +57,7 @@ constexpr int kFOffMA = kFOffNlm + kFWords * 4;                 // uint4[128 + 4
 constexpr int kFOffP = kFOffMA + (kFWords + 4) * 16;            // u32[128 + 4] prefix counts (semi | rare << 16) + total
 constexpr int kFOffNl = kFOffP + (kFWords + 4) * 4;             // u16[kFMaxLines + 8] newline positions
 constexpr int kFOffInfo = kFOffNl + (kFMaxLines + 8) * 2;       // u32[kFMaxLines] line info
-constexpr int kFOffMB = kFOffInfo + kFMaxLines * 4;             // record mode: uint4[128 + 4] {comma, open, close, -}
+constexpr int kFOffMB = kFOffInfo + kFMaxLines * 4;             // record mode: uint4[128 + 4] {comma, bracket, bracket out of turn, parity} (+ zero sentinels)
 constexpr int kFWarpSmemHist = kFOffMB;
 constexpr int kFWarpSmemRec = kFOffMB + (kFWords + 4) * 16;
 static_assert(kFWarpSmemHist % 16 == 0 && kFWarpSmemRec % 16 == 0 && kFOffNlm % 16 == 0 && kFOffMA % 16 == 0 && kFOffP % 16 == 0 &&
@@ -194,6 +203,10 @@ FFB_D uint64_t describe_fast(const uint8_t* s, int a, int b) {
   const uint64_t h = ffb_hash_packed(lo, hi, (uint32_t)len);
   const unsigned c0 = (unsigned)(lo & 0xffu);
   if (c0 == '%') {
+    // special registers start with %t %l %w %g %n, or are long enough to END in "%gridid" / "WARP_SZ" / "%ctaid.x"
+    const unsigned c1 = (unsigned)((lo >> 8) & 0xffu) - 'a';
+    if (len < 8 && !(c1 < 26u && ((1u << c1) & ((1u << ('t' - 'a')) | (1u << ('l' - 'a')) | (1u << ('w' - 'a')) | (1u << ('g' - 'a')) | (1u << ('n' - 'a'))))))
+      return ffb_op_make(FFB_OPK_REG, h);
     if (len == 6 && lo == ffb_pk("%tid.x")) return ffb_op_make(FFB_OPK_TIDX, h);
     if ((len >= 5 && (lo & 0xffffffffffull) == ffb_pk("%tid.")) || (len == 7 && (lo == ffb_pk("%laneid") || lo == ffb_pk("%warpid"))))
       return ffb_op_make(FFB_OPK_UNKNOWN, h);
@@ -283,17 +296,163 @@ FFB_D bool address_fast(const uint8_t* s, int a, int b, uint32_t* kind, uint64_t
   return true;
 }
 
+// ---- opcode memo ----------------------------------------------------------------------------------
+// PTX repeats a few hundred opcode strings ("ld.global.f32", "mad.lo.s32" ...).  classify_opcode
+// (ptx.py:99-136) depends on that string alone, so every CTA keeps a small table  text (<= 24 bytes,
+// compared exactly) -> opcode part of the meta word  in shared memory: a statement costs one probe
+// instead of a token loop.  Entries are written once and never change: a writer claims the slot's
+// state word, stores the first half of the key, then (after a fence) the half that carries the
+// value with its valid bit; a reader loads that half first.
+constexpr int kMemoSlots = 256;
+constexpr uint32_t kMemoValid = 1u << 31;
+#ifdef FFB_SIMT_EMUL
+#define FFB_COMPILER_FENCE() __asm__ __volatile__("" ::: "memory")
+#else
+#define FFB_COMPILER_FENCE() asm volatile("" ::: "memory")
+#endif
+struct MemoKey { uint32_t k0, k1, k2, k3, k4, k5, slot; };
+FFB_D void memo_key(const uint8_t* s, int p, int len, MemoKey& k) {          // 1 <= len <= 24
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + (p & ~3));
+  const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3], w4 = wp[4], w5 = wp[5], w6 = wp[6];
+  const int sh = (p & 3) * 8;
+  const int q = len >> 2;
+  const uint32_t pm = (1u << ((len & 3) * 8)) - 1u;
+  uint32_t v;
+  v = __funnelshift_r(w0, w1, sh); k.k0 = q > 0 ? v : (v & pm);
+  v = __funnelshift_r(w1, w2, sh); k.k1 = q > 1 ? v : (q == 1 ? (v & pm) : 0u);
+  v = __funnelshift_r(w2, w3, sh); k.k2 = q > 2 ? v : (q == 2 ? (v & pm) : 0u);
+  v = __funnelshift_r(w3, w4, sh); k.k3 = q > 3 ? v : (q == 3 ? (v & pm) : 0u);
+  v = __funnelshift_r(w4, w5, sh); k.k4 = q > 4 ? v : (q == 4 ? (v & pm) : 0u);
+  v = __funnelshift_r(w5, w6, sh); k.k5 = q > 5 ? v : (q == 5 ? (v & pm) : 0u);
+  uint32_t h = (k.k0 * 0x9e3779b1u) ^ (k.k1 * 0x85ebca77u) ^ (k.k2 * 0xc2b2ae3du) ^ (k.k3 * 0x27d4eb2fu) ^ (k.k4 * 0x165667b1u) ^ (k.k5 * 0xd3a2646du);
+  h ^= h >> 15;
+  k.slot = (h * 0x2c1b3c6du) >> 24;
+}
+constexpr int kMemoProbes = 8;
+FFB_D uint32_t memo_probe(const uint4* memo, const MemoKey& k) {             // value with kMemoValid set, or 0
+  uint32_t sl = k.slot;
+#pragma unroll 1
+  for (int pr = 0; pr < kMemoProbes; ++pr) {
+    const uint4 e1 = memo[2 * sl + 1];
+    FFB_COMPILER_FENCE();
+    const uint4 e0 = memo[2 * sl];
+    if ((e1.z & kMemoValid) && e1.x == k.k4 && e1.y == k.k5 && e0.x == k.k0 && e0.y == k.k1 && e0.z == k.k2 && e0.w == k.k3) return e1.z;
+    if (e1.w == 0u) break;                             // never claimed: the opcode is not in the table
+    sl = (sl + 1u) & (kMemoSlots - 1);
+  }
+  return 0u;
+}
+FFB_D uint32_t opcode_bits(const OpcodeInfo& oc) {     // the opcode's share of FfbInsRec.meta
+  return oc.cls | (oc.space << 4) | ((oc.bytes & 63u) << 7) | (oc.base << 13) | (oc.cmp << 23);
+}
+// Opcodes of 25..56 bytes (mma / tex / wmma shapes) have a table of their own: 64-byte entries
+// {14 key words, value, state}, same protocol.  Longer ones always take the token walk.
+constexpr int kLongSlots = 32, kLongProbes = 4, kLongWords = 14;
+FFB_NOINLINE uint32_t cold_long_opcode(const uint64_t* tok_key, const uint32_t* tok_val, const uint8_t* s, int p0, int p1, uint32_t* lmemo) {
+  TokTable tt;
+  tt.key = tok_key; tt.val = tok_val;
+  const int len = p1 - p0;
+  if (len > 4 * kLongWords) return opcode_bits(classify_opcode(tt, s, p0, p1)) | kMemoValid;
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + (p0 & ~3));
+  const int sh = (p0 & 3) * 8, q = len >> 2;
+  const uint32_t pm = (1u << ((len & 3) * 8)) - 1u;
+  uint32_t h = 0x811c9dc5u;
+#pragma unroll 1
+  for (int i = 0; i <= q && i < kLongWords; ++i) {
+    uint32_t v = __funnelshift_r(wp[i], wp[i + 1], sh);
+    if (i == q) v &= pm;
+    h = (h ^ v) * 0x01000193u;
+  }
+  h ^= h >> 15;
+  uint32_t sl = (h * 0x2c1b3c6du) >> 27;
+#pragma unroll 1
+  for (int pr = 0; pr < kLongProbes; ++pr) {
+    uint32_t* e = lmemo + 16 * sl;
+    const uint32_t val = e[14];
+    FFB_COMPILER_FENCE();
+    if (val & kMemoValid) {
+      bool same = true;
+#pragma unroll 1
+      for (int i = 0; i < kLongWords && same; ++i) {
+        uint32_t v = i <= q ? __funnelshift_r(wp[i < q ? i : q], wp[(i < q ? i : q) + 1], sh) : 0u;
+        if (i == q) v &= pm;
+        same = e[i] == v;
+      }
+      if (same) return val;
+    } else if (e[15] == 0u) break;
+    sl = (sl + 1u) & (kLongSlots - 1);
+  }
+  const uint32_t val = opcode_bits(classify_opcode(tt, s, p0, p1)) | kMemoValid;
+  sl = (h * 0x2c1b3c6du) >> 27;
+  for (int pr = 0; pr < kLongProbes; ++pr) {
+    uint32_t* e = lmemo + 16 * sl;
+    if (atomicCAS(e + 15, 0u, 1u) == 0u) {
+      for (int i = 0; i < kLongWords; ++i) {
+        uint32_t v = i <= q ? __funnelshift_r(wp[i < q ? i : q], wp[(i < q ? i : q) + 1], sh) : 0u;
+        if (i == q) v &= pm;
+        e[i] = v;
+      }
+      __threadfence_block();
+      e[14] = val;
+      break;
+    }
+    const uint32_t seen = e[14];
+    FFB_COMPILER_FENCE();
+    if (!(seen & kMemoValid)) break;                   // being written: leave the insert to a later statement
+    bool same = true;
+    for (int i = 0; i < kLongWords && same; ++i) {
+      uint32_t v = i <= q ? __funnelshift_r(wp[i < q ? i : q], wp[(i < q ? i : q) + 1], sh) : 0u;
+      if (i == q) v &= pm;
+      same = e[i] == v;
+    }
+    if (same) break;
+    sl = (sl + 1u) & (kLongSlots - 1);
+  }
+  return val;
+}
+// memo miss: the token walk of the exact kernel, then the insert
+FFB_NOINLINE uint32_t cold_opcode(const uint64_t* tok_key, const uint32_t* tok_val, const uint8_t* s, int p0, int p1, uint4* memo,
+                                  uint32_t k0, uint32_t k1, uint32_t k2, uint32_t k3, uint32_t k4, uint32_t k5, uint32_t slot) {
+  TokTable tt;
+  tt.key = tok_key; tt.val = tok_val;
+  const uint32_t val = opcode_bits(classify_opcode(tt, s, p0, p1)) | kMemoValid;
+  uint32_t sl = slot;
+  for (int pr = 0; pr < kMemoProbes; ++pr) {
+    uint32_t* state = reinterpret_cast<uint32_t*>(memo + 2 * sl + 1) + 3;
+    if (atomicCAS(state, 0u, 1u) == 0u) {
+      memo[2 * sl] = make_uint4(k0, k1, k2, k3);
+      __threadfence_block();
+      memo[2 * sl + 1] = make_uint4(k4, k5, val, 1u);
+      break;
+    }
+    // claimed by another lane: while its entry is still being written (most likely this very opcode, missed by
+    // many lanes at once) leave the insert to a later statement; a finished entry with this key ends the search
+    const uint4 e1 = memo[2 * sl + 1];
+    FFB_COMPILER_FENCE();
+    const uint4 e0 = memo[2 * sl];
+    if (!(e1.z & kMemoValid)) break;
+    if (e1.x == k4 && e1.y == k5 && e0.x == k0 && e0.y == k1 && e0.z == k2 && e0.w == k3) break;
+    sl = (sl + 1u) & (kMemoSlots - 1);
+  }
+  return val;
+}
+// opcode s[p0, p1) -> opcode bits of the meta word
+FFB_D uint32_t opcode_of(const TokTable& tok, uint4* memo, const uint8_t* s, int p0, int p1) {
+  const int len = p1 - p0;
+  if (len > 24) return cold_long_opcode(tok.key, tok.val, s, p0, p1, reinterpret_cast<uint32_t*>(memo + 2 * kMemoSlots)) & ~kMemoValid;
+  MemoKey k;
+  memo_key(s, p0, len, k);
+  uint32_t val = memo_probe(memo, k);
+  if (!val) val = cold_opcode(tok.key, tok.val, s, p0, p1, memo, k.k0, k.k1, k.k2, k.k3, k.k4, k.k5, k.slot);
+  return val & ~kMemoValid;
+}
+
 template <int kMode>
-FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, int kb, int ke, Emit& em) {
+FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, uint4* memo, int kb, int ke, Emit& em) {
   const int n = ke - kb;
   const int w0 = kb >> 5, sh = kb & 31;
   const uint64_t valid = low_mask(n);
-  uint64_t BL, DT;
-  {
-    const uint4 a0 = MA[w0], a1 = MA[w0 + 1], a2 = MA[w0 + 2];
-    BL = win64(a0.z, a1.z, a2.z, sh) & valid;
-    DT = win64(a0.w, a1.w, a2.w, sh) & valid;
-  }
+  const uint64_t BL = win64(MA[w0].z, MA[w0 + 1].z, MA[w0 + 2].z, sh) & valid;
   // ---- predicate  ^@(!?%[\w$]+)\s+  (ptx.py:42) ----
   int o0 = 0, p0 = 0, p1 = 0;
   bool has_pred = false, neg = false;
@@ -316,14 +475,16 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
   const uint64_t after = BL & high_mask(o0);
   if (!after && n > 64) return false;
   const int o1 = after ? __ffsll((long long)after) - 1 : n;
-  uint64_t D = DT & low_mask(o1) & high_mask(o0);
-  uint32_t base = TB_NONE, elem_code = 0, vec = 0, space = 0, cmp = 0, flags = 0;
+  uint32_t ob;
   if (kMode == 1) {
     // histogram mode needs the class only: the first token, whether the last one is "sync", and - for the
-    // arithmetic bases and sqrt alone - the type / approx tokens in between (ptx.py:104-128)
+    // arithmetic bases and sqrt alone - the type / approx tokens in between (ptx.py:104-128).  Shorter than a
+    // probe of the memo (measured: 481 vs 460 GB/s).
+    uint64_t D = win64(MA[w0].w, MA[w0 + 1].w, MA[w0 + 2].w, sh) & valid & low_mask(o1) & high_mask(o0);
+    uint32_t flags = 0;
     const int t0e = D ? __ffsll((long long)D) - 1 : o1;
     const int len0 = t0e - o0;
-    base = (len0 > 8 ? 0u : tok_lookup(em.tok, load_packed(s, kb + o0, len0))) & 31u;
+    const uint32_t base = (len0 > 8 ? 0u : tok_lookup(em.tok, load_packed(s, kb + o0, len0))) & 31u;
     if (D) {
       const int ld = 63 - __clzll((long long)D);
       if (o1 - ld - 1 == 4 && load_packed(s, kb + ld + 1, 4) == ffb_pk("sync")) flags |= 8u;
@@ -344,53 +505,36 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
         }
       }
     }
+    ob = finish_opcode(base, 0, 0, 0, 0, flags).cls;
   } else {
-    int ts = o0, ti = 0;
-    for (;;) {
-      const int te = D ? __ffsll((long long)D) - 1 : o1;
-      const int len = te - ts;
-      const uint32_t v = len > 8 ? 0u : tok_lookup(em.tok, load_packed(s, kb + ts, len));
-      flags &= ~8u;
-      if (ti == 0) base = v & 31u;
-      else {
-        const uint32_t ec = (v >> 5) & 7u;
-        if (ec) elem_code = ec;
-        flags |= (v >> 8) & 3u;
-        const uint32_t vc = (v >> 10) & 3u;
-        if (vc) vec = vc;
-        if (v & (1u << 12)) flags |= 8u;
-        const uint32_t sp = (v >> 13) & 7u;
-        if (sp && !space) space = sp;
-      }
-      if (v & (1u << 16)) flags |= 4u;
-      if (!cmp) cmp = (v >> 17) & 7u;
-      if (!D) break;
-      D &= D - 1;
-      ts = te + 1; ++ti;
-    }
+    // record mode: one probe of the CTA's opcode memo (ptx.py:99-136, :64-76)
+    ob = opcode_of(em.tok, memo, s, kb + o0, kb + o1);
   }
-  const OpcodeInfo oc = finish_opcode(base, elem_code, vec, space, cmp, flags);
+  OpcodeInfo oc;
+  oc.cls = ob & 15u; oc.space = (ob >> 4) & 7u; oc.bytes = (ob >> 7) & 63u; oc.base = (ob >> 13) & 31u; oc.cmp = (ob >> 23) & 7u;
   if (kMode == 2) {
     // ---- operands: top-level commas (ptx.py:144-162) ----
     // a second set of windows, anchored at the end of the opcode, so that the operand list may
     // itself be 64 bytes long (mma / tex / vector forms with a long opcode in front)
     const int ko = kb + o1, m = n - o1;
     if (m > 64) return false;
-    uint64_t BO, CM, OP, CL;
+    // phase T left {commas, brackets, brackets out of turn, parity} in MB; the parity in front of the list is the
+    // list's depth 0 (the kernel body itself sits inside a brace)
+    uint64_t BO, CM, XX, BD, IN;
     {
       const int wo = ko >> 5, so = ko & 31;
       const uint64_t R = low_mask(m);
-      const uint4 a0 = MA[wo], a1 = MA[wo + 1], a2 = MA[wo + 2];
       const uint4 b0 = MB[wo], b1 = MB[wo + 1], b2 = MB[wo + 2];
-      BO = win64(a0.z, a1.z, a2.z, so) & R;
-      CM = win64(b0.x, b1.x, b2.x, so) & R; OP = win64(b0.y, b1.y, b2.y, so) & R; CL = win64(b0.z, b1.z, b2.z, so) & R;
+      BO = win64(MA[wo].z, MA[wo + 1].z, MA[wo + 2].z, so) & R;
+      CM = win64(b0.x, b1.x, b2.x, so) & R; XX = win64(b0.y, b1.y, b2.y, so) & R; BD = win64(b0.z, b1.z, b2.z, so) & R;
+      IN = win64(b0.w, b1.w, b2.w, so);
     }
     const uint64_t NB = ~BO & low_mask(m);
     uint64_t inside = 0;
-    if (OP | CL) {                                    // brackets must alternate open / close (depth 0 or 1)
-      const uint64_t X = OP | CL, incl = prefix_xor64(X), excl = incl ^ X;
-      if ((OP & excl) || (CL & ~excl) || (__popcll(X) & 1)) return false;
-      inside = incl;
+    if (XX) {                                         // brackets must alternate open / close (depth 0 or 1) and balance
+      if ((IN ^ XX) & 1ull) { IN = ~IN; BD = XX & ~BD; }
+      if (BD || ((IN >> (m - 1)) & 1ull)) return false;
+      inside = IN;
     }
     const uint64_t C0 = CM & ~inside;
     const bool is_mem = oc.cls == FFB_CLS_MEMLOAD || oc.cls == FFB_CLS_MEMSTORE;
@@ -400,11 +544,10 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
     int count = 0, as = -1, ae = -1, last_s = -1, last_e = -1;
     bool extra_reg = false, dst_reg = false;
     {
-      uint64_t rem = C0;
-      int from = 0;
+      uint64_t rem = C0, nb = NB;                     // commas and non-blank bytes not yet consumed
       for (;;) {
-        const int to = rem ? __ffsll((long long)rem) - 1 : m;
-        const uint64_t seg = NB & low_mask(to) & high_mask(from);
+        const uint64_t below = (rem & (0ull - rem)) - 1ull;       // bits in front of the next comma (all bits when none is left)
+        const uint64_t seg = nb & below;
         if (!seg) {
           if (C0) return false;                       // empty operand between commas: the walk drops it
           break;
@@ -421,15 +564,15 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
         last_s = a; last_e = b;
         ++count;
         if (!rem) break;
+        nb &= ~((below << 1) | 1ull);                 // drop the operand and its comma
         rem &= rem - 1;
-        from = to + 1;
       }
     }
     uint32_t addr_kind = FFB_ADDR_ABSENT;
     if (is_mem) {
       if (as >= 0) {
         const uint64_t span = low_mask(ae - ko) & high_mask(as - ko);
-        const bool canonical = ae - as <= 16 && !(BO & span) && ((OP | CL) & span) == ((1ull << (as - ko)) | (1ull << (ae - ko - 1)));
+        const bool canonical = ae - as <= 16 && !(BO & span) && (XX & span) == ((1ull << (as - ko)) | (1ull << (ae - ko - 1)));
         if (!canonical || !address_fast(s, as, ae, &addr_kind, &rec.aux)) {
           const AddrDesc ad = cold_describe_address(s, as, ae);
           addr_kind = ad.kind; rec.aux = ad.desc;
@@ -441,8 +584,7 @@ FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, in
     rec.off = (uint32_t)(em.abase + kb - em.seg_begin);
     rec.len = (uint32_t)(NB ? o1 + 64 - __clzll((long long)NB) : o1);
     rec.pred = has_pred ? hash_span(s, p0, p1) : 0ull;
-    rec.meta = oc.cls | (oc.space << 4) | ((oc.bytes & 63u) << 7) | (oc.base << 13) | ((has_pred ? 1u : 0u) << 18) |
-               ((neg ? 1u : 0u) << 19) | ((uint32_t)(count > 7 ? 7 : count) << 20) | (oc.cmp << 23) | (addr_kind << 26) |
+    rec.meta = ob | ((has_pred ? 1u : 0u) << 18) | ((neg ? 1u : 0u) << 19) | ((uint32_t)(count > 7 ? 7 : count) << 20) | (addr_kind << 26) |
                ((dst_reg ? 1u : 0u) << 28) | ((extra_reg ? 1u : 0u) << 29);
     if (em.ins_at < em.ins_limit) {
       em.a->ins[em.ins_at] = rec;
@@ -600,6 +742,7 @@ lex_fast_kernel(LexArgs a) {
   __shared__ uint8_t s_cls[256];
   __shared__ uint64_t s_tok_key[256];
   __shared__ uint32_t s_tok_val[256];
+  __shared__ uint4 s_memo[2 * kMemoSlots + 4 * kLongSlots];     // short-opcode table, then the long-opcode table
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   uint8_t* s = smem_raw + (size_t)wid * (kRecords ? kFWarpSmemRec : kFWarpSmemHist);
@@ -611,6 +754,7 @@ lex_fast_kernel(LexArgs a) {
   uint16_t* nl = reinterpret_cast<uint16_t*>(s + kFOffNl);
   uint32_t* linfo = reinterpret_cast<uint32_t*>(s + kFOffInfo);
   for (int c = threadIdx.x; c < 256; c += (int)blockDim.x) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
+  for (int c = threadIdx.x; c < 2 * kMemoSlots + 4 * kLongSlots; c += (int)blockDim.x) s_memo[c] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   for (int c = threadIdx.x; c < kNumTokDefs; c += (int)blockDim.x) {
     const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
@@ -669,6 +813,12 @@ lex_fast_kernel(LexArgs a) {
       __syncwarp();
 
       // ================= M: load, masks, stage =================
+      // the tile after this one starts its way from DRAM to L2 now (one 128-byte line per lane): all warps of the
+      // barrier-paced CTA reach their loads together, nothing else hides that latency
+      if (kPrefetch) {
+        const int64_t pf = abase + kFTile + (int64_t)lane * 128;
+        if (pf + 128 <= a.n_bytes && pf < seg_end) FFB_PREFETCH_L2(a.text + pf);
+      }
       uint32_t badacc = 0;
 #pragma unroll 1
       for (int v0 = 0; v0 < 8; v0 += 2) {                        // rolled on purpose: code size (see the note on cold paths)
@@ -761,6 +911,25 @@ lex_fast_kernel(LexArgs a) {
             if (at < kFMaxLines) nl[at] = (uint16_t)(lane * 128 + 32 * k + bit);
             ++at;
           }
+        }
+      }
+      if (kRecords) {
+        // bracket parity by a prefix-xor over the whole tile (brackets alternate open / close in everything the
+        // window parser accepts): MB becomes {commas, brackets, brackets that do not alternate from parity 0,
+        // parity}.  A statement reads the parity in front of its operand list (the kernel body itself sits inside
+        // a brace) and takes everything relative to it.
+        uint4 b[4];
+        uint32_t X[4], par = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { b[k] = MB[4 * lane + k]; X[k] = b[k].y | b[k].z; par ^= (uint32_t)__popc(X[k]); }
+        uint32_t carry = (uint32_t)__popc(__ballot_sync(kFull, par & 1u) & lt_mask) & 1u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t px = X[k];
+          px ^= px << 1; px ^= px << 2; px ^= px << 4; px ^= px << 8; px ^= px << 16;
+          const uint32_t incl = px ^ (0u - carry), excl = incl ^ X[k];
+          MB[4 * lane + k] = make_uint4(b[k].x, X[k], (b[k].y & excl) | (b[k].z & ~excl), incl);
+          carry ^= (uint32_t)__popc(X[k]) & 1u;
         }
       }
       const int n_real = total_nl < kFMaxLines ? total_nl : kFMaxLines;
@@ -905,7 +1074,7 @@ lex_fast_kernel(LexArgs a) {
           if (kind == FK_STMT) {
             em.ins_at = my_ins;
             em.line = line_no + (uint32_t)li;
-            slow = !fast_statement<kMain>(s, MA, MB, kb, ke, em);
+            slow = !fast_statement<kMain>(s, MA, MB, s_memo, kb, ke, em);
           }
           const unsigned slm = __ballot_sync(kFull, slow);
           if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | ((int)(my_ins - ins_base - tile_ins0) << 8));
@@ -963,7 +1132,7 @@ lex_fast_kernel(LexArgs a) {
           const uint32_t inf = linfo[li];
           em.ins_at = ins_base + tile_ins0 + (ent >> 8);
           em.line = line_no + (uint32_t)li;
-          slow = !fast_statement<kMain>(s, MA, MB, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
+          slow = !fast_statement<kMain>(s, MA, MB, s_memo, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
         }
         const unsigned slm = __ballot_sync(kFull, slow);
         if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)ent;
