@@ -47,6 +47,11 @@ def parse_args():
     ap.add_argument("--lex-flags", type=int, default=0, help="FFB_LEX_* bits for A/B runs (2 = no lock-step CTAs)")
     ap.add_argument("--unfused", action="store_true", help="score + front as two kernels with the [K,S,J,C] grid in HBM "
                     "(ffb_predict_grid -> ffb_skyline_groups) instead of the fused ffb_explore_groups")
+    ap.add_argument("--workload", default="analysis", choices=["analysis", "front1e9", "front1e9_3obj", "grid_c3", "c1_latency"],
+                    help="analysis = the headline step (BASELINE configs[3] x [2]); the others are BASELINE configs[4], [2], [0] (bench_extra.py)")
+    ap.add_argument("--candidates", type=float, default=1e9, help="front1e9*: candidates of the whole set (split over the ranks)")
+    ap.add_argument("--e2e-candidates", type=float, default=float(1 << 28), help="front1e9*: candidates per rank of the host-buffer (e2e) leg")
+    ap.add_argument("--weak-front", action="store_true", help="front1e9*: --candidates per GPU instead of in total")
     return ap.parse_args()
 
 
@@ -84,62 +89,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-# --------------------------------------------------------------------------- CPU legs (oracle)
-def _cpu_score_front(args):
-    """Oracle port of score + front for a slice of kernels (one worker)."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import flipflop_oracle as orc
-    from paper_2601_13345_b200 import specs
-    feat, res, shp, tie = args
-    a, p = specs.default_architecture(), specs.default_calibration()
-    t, e = orc.score_grid_numpy(feat, res, orc.arch_dict(a), orc.cal_dict(p), shp, CAPS)
-    n_front = 0
-    for k in range(feat.shape[0]):
-        idx, _ = orc.pareto_indices(e[k].reshape(-1), t[k].reshape(-1), tie=tie, rho=RHO)
-        n_front += len(idx)
-    return feat.shape[0] * shp.shape[0] * CAPS.size, n_front
-
-
-def _cpu_lex(args):
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import flipflop_oracle as orc
-    text, offs = args
-    n = 0
-    for i in range(len(offs) - 1):
-        orc.kernel_feature_row(text[offs[i]:offs[i + 1]].decode("ascii"))
-        n += int(offs[i + 1] - offs[i])
-    return n
-
-
-def cpu_sample(feat, res, shp, tie, corpus, workers: int, k_score: int, lex_bytes: int):
-    """Times the oracle on a bounded sample; returns (points/s, bytes/s, description)."""
-    import multiprocessing as mp
-    chunks = [c for c in np.array_split(np.arange(min(k_score, feat.shape[0])), max(workers, 1)) if c.size]
-    jobs = [(feat[c], res[c], shp, tie) for c in chunks]
-    lex_jobs = []
-    if corpus is not None:
-        text, offs = corpus
-        k = int(np.searchsorted(offs, lex_bytes, side="right"))
-        k = max(k, min(workers + 1, len(offs)))
-        bounds = np.linspace(0, k - 1, max(workers, 1) + 1).astype(int)
-        lex_jobs = [(text, offs[bounds[i]:bounds[i + 1] + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(max(workers, 1)) as pool:
-        t0 = time.perf_counter()
-        pts = sum(r[0] for r in pool.map(_cpu_score_front, jobs))
-        t_score = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        nbytes = sum(pool.map(_cpu_lex, lex_jobs)) if lex_jobs else 0
-        t_lex = time.perf_counter() - t0
-    return pts, t_score, nbytes, t_lex
-
-
 # --------------------------------------------------------------------------- main
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload != "analysis":
+        import bench_extra
+        if args.impl == "reference":
+            out = bench_extra.reference_arm_extra(args)
+        elif args.workload in ("front1e9", "front1e9_3obj"):
+            out = bench_extra.run_front(args, args.workload.endswith("3obj"), ClockSampler)
+        elif args.workload == "grid_c3":
+            out = bench_extra.run_grid_c3(args, ClockSampler)
+        else:
+            out = bench_extra.run_c1_latency(args, ClockSampler)
+        if out is not None:
+            print(json.dumps(out))
+        return
     if args.impl == "reference":
         return reference_arm(args, rank, world)
 
@@ -328,6 +296,17 @@ def main():
     clocks = sampler.stop() if rank == 0 else None
     ms_e2e, _, _ = run(False, max(3, args.steps // 2), 2)
     e2e_steps = max(3, args.steps // 2)
+    # the floor of the e2e leg: the same pinned host -> device copy of the corpus with nothing else running
+    h2d_alone_ms = None
+    if corpus is not None and lex_state.host_text is not None:
+        torch.cuda.synchronize()
+        c0, c1 = ev(), ev()
+        c0.record()
+        for _ in range(3):
+            corpus.text.copy_(lex_state.host_text, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        h2d_alone_ms = c0.elapsed_time(c1) / 3
 
     # ---- K1 alone, histogram mode (north_star leg 1: text -> per-kernel class histograms) ----
     hist_ms, path_counts = None, None
@@ -433,17 +412,27 @@ def main():
                 "all_kernels": {k: {kk: vv for kk, vv in v.items() if kk != "bytes"} for k, v in kernels.items()}}
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and corpus is not None:
+        # the CPU implementation (the reference itself when its copy travelled, else the oracle port) runs the SAME path
+        # on a bounded sample of the same kernels: lex + CFG + features + 3248 configs scored + front, per kernel;
+        # its fronts are compared with the ones the GPU step produced for those kernels
+        import bench_extra
         workers = os.cpu_count() or 1
-        k_cpu = min(K, 1000 * workers)
-        pts, t_score, nb, t_lex = cpu_sample(feat_np, res_np, shp_xy, tie_np,
-                                            corpus.host_sample() if corpus is not None else None,
-                                            workers, k_cpu, lex_bytes=2_500_000 * workers)
-        cpu = {"value": pts / t_score, "unit": "configs/s", "cores": workers, "kind": "port",
-               "sample": f"oracle (numpy score_grid + sort-sweep front) on {k_cpu} kernels x {G} configs = {pts} points, "
-                         f"{workers} processes, {t_score:.1f} s"
-                         + (f"; lexer+dataflow oracle on {nb / 1e6:.1f} MB in {t_lex:.1f} s" if nb else ""),
-               "lex_value": (nb / t_lex / 1e9) if nb else None, "lex_unit": "GB/s"}
+        text, offs = corpus.host_sample()
+        pick = bench_extra.cpu_sample_kernels(offs, workers, 0)
+        n_cpu = len(pick)
+        srcs = [text[offs[k]:offs[k + 1]].decode("ascii") for k in pick]
+        r = bench_extra.cpu_analysis(srcs, [int(res_np[k, 1]) for k in pick], workers)
+        fo_res, fi_res = front_bufs[3].cpu().numpy(), fi.cpu().numpy()
+        for k, fr in zip(pick, r["fronts"]):
+            mine = fi_res[int(fo_res[k]): int(fo_res[k]) + int(fn0_host[k])]
+            got = [(int(shp_xy[i // C, 0]), int(shp_xy[i // C, 1]), float(CAPS[i % C])) for i in mine]
+            assert got == fr, f"front of kernel {k} differs from the CPU {r['kind']} implementation"
+        cpu = {"value": r["points"] / r["seconds"], "unit": "configs/s", "cores": r["workers"], "kind": r["kind"],
+               "sample": f"{n_cpu} of this step's kernels ({r['bytes'] / 1e6:.2f} MB of PTX; {bench_extra.SAMPLE_NOTE}) through the whole path - lex, "
+                         f"CFG, features, {G} configs scored, front - {r['workers']} processes, {r['seconds']:.1f} s; fronts identical to the GPU step's",
+               "lex_value": r["bytes"] / r["seconds"] / 1e9, "lex_unit": "GB/s (text per second of the whole path)",
+               "fronts_checked": n_cpu}
 
     out = {
         "metric": "configs_scored_per_sec", "value": value, "unit": "configs/s", "n_gpus": world,
@@ -467,7 +456,7 @@ def main():
                                           + h_front_n.numel() * 4 + h_front_off.numel() * 8) * world,
                 "pipeline": (f"{len(e2e['regions'])} chunks of <= {args.e2e_chunk_mb} MB: upload, K1+K1b, K2+K3, K4 and the front read-back overlap"
                              if e2e.get("regions") else "none"),
-                "ms_per_step": ms_e2e / e2e_steps, "steps": e2e_steps},
+                "ms_per_step": ms_e2e / e2e_steps, "steps": e2e_steps, "h2d_alone_ms": h2d_alone_ms},
         "roofline": roofline, "cpu_baseline": cpu,
     }
     print(json.dumps(out))
@@ -476,50 +465,35 @@ def main():
 
 
 def reference_arm(args, rank, world):
-    """CPU arm: the oracle port of the same pass on all host cores, bounded sample per step."""
+    """CPU arm of the headline workload: the reference's own code (oracle/_ref/ptxwatt; the oracle port when that copy is
+    absent) runs the same path per kernel - lex, CFG + trips, features, 464 shapes x 7 caps scored, front at rho - on a
+    bounded sample of the same generated kernels per step, one process per host core."""
     if rank != 0:
         return
-    from paper_2601_13345_b200 import specs, synth
-    try:
-        from paper_2601_13345_b200 import corpus as corpus_mod
-    except ImportError:
-        corpus_mod = None
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import flipflop_oracle as orc  # noqa: F401
-    import ctypes  # enumerate shapes without a GPU: pure host entry point of libffb
-    from paper_2601_13345_b200 import native
-    from paper_2601_13345_b200.specs import pack_spec
-    a, p = specs.default_architecture(), specs.default_calibration()
-    ad = orc.arch_dict(a)
-    cfgs = orc.enumerate_configs(ad, 0, DIMS, None)
-    shp_xy = np.array([(bx, by) for bx, by, _ in cfgs], dtype=np.int32)
-    J, C = shp_xy.shape[0], CAPS.size
-    G = J * C
-    order = np.lexsort((shp_xy[:, 1], shp_xy[:, 0]))
-    rank_of_shape = np.empty(J, dtype=np.int64)
-    rank_of_shape[order] = np.arange(J)
-    tie_np = (rank_of_shape[:, None] * C + np.arange(C)[None, :]).reshape(-1).astype(np.int32)
+    import bench_extra
+    from paper_2601_13345_b200 import synth
     workers = os.cpu_count() or 1
-    k_step = 160 * workers
-    feat_np, res_np = synth.feature_rows(seed=3, n_kernels=k_step)
-    res_np[:, 0] = 0
-    corpus_sample = None
-    if corpus_mod is not None:
-        corpus_sample = synth.ptx_corpus(4, max(workers, int(workers * 2_500_000 / 40_000)))
-    tot_pts, tot_t, tot_b, tot_tl = 0, 0.0, 0, 0.0
+    text, offs = synth.ptx_corpus(4, 1200)                       # the base kernels of the GPU arm's corpus (corpus.bench_corpus)
+    _, res_np = synth.feature_rows(seed=3, n_kernels=KERNELS_PER_RANK)
+    tot_pts, tot_t, tot_b = 0, 0.0, 0
     for i in range(args.warmup + args.steps):
-        pts, t_score, nb, t_lex = cpu_sample(feat_np, res_np, shp_xy, tie_np, corpus_sample, workers, k_step, 10**9)
+        pick = bench_extra.cpu_sample_kernels(offs, workers, i)   # another sample of the corpus every step
+        n = len(pick)
+        srcs = [text[offs[k]:offs[k + 1]].decode("ascii") for k in pick]
+        r = bench_extra.cpu_analysis(srcs, [int(res_np[k, 1]) for k in pick], workers)
         if i >= args.warmup:
-            tot_pts += pts; tot_t += t_score + t_lex; tot_b += nb; tot_tl += t_lex
+            tot_pts += r["points"]; tot_t += r["seconds"]; tot_b += r["bytes"]
     value = tot_pts / tot_t
+    G = tot_pts // max(args.steps * n, 1)
+    sample = (f"{n} generated kernels per step ({tot_b / max(args.steps, 1) / 1e6:.2f} MB of PTX lexed, {G} configs each scored and ranked; "
+              f"{bench_extra.SAMPLE_NOTE}), {r['workers']} processes")
     out = {"impl": "reference", "metric": "configs_scored_per_sec", "value": value, "unit": "configs/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"oracle port of the same pass, bounded sample per step: {k_step} kernels x {G} configs"
-                                  + (f" + {tot_b / max(args.steps, 1) / 1e6:.1f} MB PTX lexed" if tot_b else "")},
-           "ptx_gb_per_s": (tot_b / tot_tl / 1e9) if tot_b else None,
-           "cpu_baseline": {"value": value, "unit": "configs/s", "cores": workers, "kind": "port",
-                            "sample": f"{k_step} kernels x {G} configs per step, {workers} processes"},
+           "config": {"workload": "full FlipFlop analysis (BASELINE configs[3] x configs[2] grid) on the host cores, bounded sample per step: " + sample,
+                      "kernels_per_step": n, "shapes": 464, "caps": 7, "specs": 1, "same_path_per_kernel": True},
+           "ptx_gb_per_s": tot_b / tot_t / 1e9,
+           "cpu_baseline": {"value": value, "unit": "configs/s", "cores": r["workers"], "kind": r["kind"], "sample": sample},
            "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
