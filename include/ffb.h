@@ -242,7 +242,7 @@ typedef struct {
 } FfbSpanRec;
 
 /* Optional `.reg` declaration records (ptx.py:244-248), FFB_MAX_DECLS per segment. */
-#define FFB_MAX_DECLS 32
+#define FFB_MAX_DECLS 256
 typedef struct { uint32_t cls_off, cls_len; uint64_t count; } FfbDeclRec;
 
 typedef struct {

@@ -53,6 +53,21 @@ def _clean_span(raw: bytes) -> str:
     return txt.strip()
 
 
+def _top_level_split(text: str) -> tuple:
+    """Operand list -> operands, split at commas outside [..] {..} (..) (ptx.py:144-162); empty pieces are dropped."""
+    parts, depth, start = [], 0, 0
+    for i, ch in enumerate(text):
+        if ch in "[{(":
+            depth += 1
+        elif ch in "]})":
+            depth -= 1
+        elif ch == "," and depth == 0:
+            parts.append(text[start:i].strip())
+            start = i + 1
+    parts.append(text[start:].strip())
+    return tuple(q for q in parts if q)
+
+
 def _slice(src: bytes, off: int, length: int) -> str:
     raw = src[off: off + length]
     if b"\n" in raw or b"/" in raw:
@@ -114,9 +129,15 @@ def parse_ptx(source: str, kernel_name: str | None = None) -> PtxModule:
     for r, sp in zip(ins, spans):
         meta = int(r["meta"])
         n_ops = int(sp["n_ops"])
+        ops = tuple(_slice(src, int(sp["op_off"][i]), int(sp["op_len"][i])) for i in range(min(n_ops, _corpus.MAX_SPAN_OPS)))
         if n_ops > _corpus.MAX_SPAN_OPS:
-            raise CapacityExceeded(f"statement at line {int(r['line'])} has {n_ops} operands (limit {_corpus.MAX_SPAN_OPS})")
-        ops = tuple(_slice(src, int(sp["op_off"][i]), int(sp["op_len"][i])) for i in range(n_ops))
+            # the span record holds 12 operands; the rest of the list is cut out of the statement's own text (device
+            # offsets: the last recorded operand up to the statement's end) at its top-level commas (ptx.py:144-162)
+            last = _corpus.MAX_SPAN_OPS - 1
+            tail = _top_level_split(_clean_span(src[int(sp["op_off"][last]): int(r["off"]) + int(r["len"])]))
+            ops = ops[:last] + tail
+            if len(ops) != n_ops:
+                raise CapacityExceeded(f"statement at line {int(r['line'])}: {n_ops} operands on the device, {len(ops)} in the text")
         pred = _slice(src, int(sp["pred_off"]), int(sp["pred_len"])) if (meta >> 18) & 1 else None
         instructions.append(Instruction(
             opcode=_slice(src, int(sp["opc_off"]), int(sp["opc_len"])),

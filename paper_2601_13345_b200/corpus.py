@@ -21,7 +21,7 @@ SEG_DTYPE = np.dtype([("status", "<u4"), ("n_instr", "<u4"), ("n_labels", "<u4")
 INS_DTYPE = np.dtype([("meta", "<u4"), ("line", "<u4"), ("off", "<u4"), ("len", "<u4"), ("pred", "<u8"),
                       ("aux", "<u8"), ("op", "<u8", (4,))])
 LABEL_DTYPE = np.dtype([("hash", "<u8"), ("index", "<u4"), ("off", "<u4")])
-MAX_SPAN_OPS, MAX_DECLS = 12, 32
+MAX_SPAN_OPS, MAX_DECLS = 12, 256
 SPAN_DTYPE = np.dtype([("pred_off", "<u4"), ("pred_len", "<u4"), ("opc_off", "<u4"), ("opc_len", "<u4"),
                        ("n_ops", "<u4"), ("reserved", "<u4", (3,)), ("op_off", "<u4", (MAX_SPAN_OPS,)),
                        ("op_len", "<u4", (MAX_SPAN_OPS,))])

@@ -18,6 +18,7 @@
 // 4096-point chunks are appended to a compact buffer and reduced again until one group is
 // left; exact because strict dominance is transitive.
 #include "ffb_common.cuh"
+#include <stdlib.h>
 
 #include <math.h>
 #include <string.h>
@@ -503,6 +504,121 @@ Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie, bool h
   return p;
 }
 
+// ---- streaming pre-filter of one huge candidate set (two objectives) --------------------------------
+// Two coalesced passes over (e, t) take the set from n to roughly n / kPreBuckets + the neighbourhood of the
+// front before any sorting starts: pass 1 leaves min t per e-bucket (any monotone bucketing of e is valid, the
+// range comes from a sample and out-of-range values clamp to the edge buckets), an exclusive prefix-min over
+// the buckets follows, pass 2 keeps a candidate unless a STRICTLY lower bucket holds a strictly smaller t -
+// i.e. unless it is provably dominated (explorer.py:122-140: drop iff some j has e_j < e_i and t_j < t_i).
+// NaNs neither dominate nor get dropped.  Survivors are compacted with their ids.
+constexpr int kPreBuckets = 4096;
+constexpr int kPreThreads = 512;
+struct PreArgs {
+  const double* e; const double* t; const uint64_t* id;
+  int64_t n;
+  double* range;                    // {lo, scale}
+  unsigned long long* gmin;         // [kPreBuckets] min t per bucket, later the exclusive prefix-min
+  double* out_e; double* out_t; uint64_t* out_id;
+  int64_t out_cap;
+  unsigned long long* out_count;
+  uint32_t* overflow;
+};
+FFB_D int pre_bucket(double ev, double lo, double scale) {
+  const double x = (ev - lo) * scale;
+  if (!(x > 0.0)) return 0;                                   // below the sampled range, or NaN
+  return x >= (double)(kPreBuckets - 1) ? kPreBuckets - 1 : (int)x;
+}
+__global__ void __launch_bounds__(1024) pre_range_kernel(PreArgs a) {
+  __shared__ double s_lo[32], s_hi[32];
+  const int64_t m = a.n < 65536 ? a.n : 65536;
+  const int64_t stride = a.n / m;                             // sample spread over the whole set
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const double v = a.e[i * stride];
+    if (v > -INFINITY && v < INFINITY) { lo = v < lo ? v : lo; hi = v > hi ? v : hi; }
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    const double ol = __shfl_xor_sync(0xffffffffu, lo, d), oh = __shfl_xor_sync(0xffffffffu, hi, d);
+    lo = ol < lo ? ol : lo; hi = oh > hi ? oh : hi;
+  }
+  if ((threadIdx.x & 31) == 0) { s_lo[threadIdx.x >> 5] = lo; s_hi[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = s_lo[w] < lo ? s_lo[w] : lo; hi = s_hi[w] > hi ? s_hi[w] : hi; }
+    const double span = hi - lo;
+    a.range[0] = lo < INFINITY ? lo : 0.0;
+    a.range[1] = (span > 0.0 && span < INFINITY) ? (double)kPreBuckets / span : 0.0;
+  }
+  for (int b = threadIdx.x; b < kPreBuckets; b += blockDim.x) a.gmin[b] = ~0ull;
+}
+__global__ void __launch_bounds__(kPreThreads) pre_min_kernel(PreArgs a) {
+  __shared__ unsigned long long s_min[kPreBuckets];
+  for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads) s_min[b] = ~0ull;
+  __syncthreads();
+  const double lo = a.range[0], scale = a.range[1];
+  for (int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kPreThreads) {
+    const double ev = a.e[i], tv = a.t[i];
+    if (ev != ev || tv != tv) continue;
+    const int b = pre_bucket(ev, lo, scale);
+    const unsigned long long tb = (unsigned long long)ordered_bits(tv);
+    if (tb < s_min[b]) atomicMin(&s_min[b], tb);            // the plain read only spares atomics that cannot win
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads)
+    if (s_min[b] != ~0ull) atomicMin(&a.gmin[b], s_min[b]);
+}
+__global__ void __launch_bounds__(1024) pre_prefix_kernel(PreArgs a) {
+  // exclusive prefix-min over kPreBuckets values: 4 per thread, warp scan, scan of the warp totals
+  __shared__ unsigned long long s_w[32];
+  const int tid = threadIdx.x;
+  unsigned long long v[4], run = ~0ull;
+  for (int k = 0; k < 4; ++k) { v[k] = a.gmin[4 * tid + k]; }
+  unsigned long long tot = v[0] < v[1] ? v[0] : v[1];
+  tot = v[2] < tot ? v[2] : tot; tot = v[3] < tot ? v[3] : tot;
+  unsigned long long incl = tot;
+  for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, d); if ((tid & 31) >= d && o < incl) incl = o; }
+  if ((tid & 31) == 31) s_w[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    unsigned long long w = s_w[tid], wi = w;
+    for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, d); if (tid >= d && o < wi) wi = o; }
+    const unsigned long long ex = __shfl_up_sync(0xffffffffu, wi, 1);
+    s_w[tid] = tid == 0 ? ~0ull : ex;
+  }
+  __syncthreads();
+  unsigned long long before = __shfl_up_sync(0xffffffffu, incl, 1);
+  if ((tid & 31) == 0) before = ~0ull;
+  run = before < s_w[tid >> 5] ? before : s_w[tid >> 5];
+  for (int k = 0; k < 4; ++k) { a.gmin[4 * tid + k] = run; run = v[k] < run ? v[k] : run; }
+}
+__global__ void __launch_bounds__(kPreThreads) pre_filter_kernel(PreArgs a) {
+  __shared__ unsigned long long s_pm[kPreBuckets];
+  for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads) s_pm[b] = a.gmin[b];
+  __syncthreads();
+  const double lo = a.range[0], scale = a.range[1];
+  const int lane = threadIdx.x & 31;
+  const int64_t step = (int64_t)gridDim.x * kPreThreads;
+  const int64_t n_round = (a.n + step - 1) / step * step;     // whole warps take part in every ballot
+  for (int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x; i < n_round; i += step) {
+    bool keep = false;
+    double ev = 0.0, tv = 0.0;
+    if (i < a.n) {
+      ev = a.e[i]; tv = a.t[i];
+      keep = ev != ev || tv != tv || !(s_pm[pre_bucket(ev, lo, scale)] < (unsigned long long)ordered_bits(tv));
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(a.out_count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const int64_t at = (int64_t)base + __popc(m & ((1u << lane) - 1u));
+      if (at < a.out_cap) { a.out_e[at] = ev; a.out_t[at] = tv; a.out_id[at] = a.id ? a.id[i] : (uint64_t)i; }
+      else *a.overflow = 1u;
+    }
+  }
+}
+
 int32_t launch_groups(FfbContext* ctx, SkyArgs a, int64_t n_groups, cudaStream_t stream) {
   Plan p = plan_groups(ctx, a.group_size, a.tie != nullptr, a.id != nullptr);
   a.resident = p.resident;
@@ -580,7 +696,7 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   if (work_cap < cap_front) work_cap = cap_front;
   // scratch: two ping-pong triples + counters/status
   const size_t tri = (size_t)work_cap * (d_occ ? 32 : 24);
-  int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 2 * tri + 256);
+  int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 2 * tri + 256 + (size_t)kPreBuckets * 8 + 64);
   if (rc) return rc;
   char* base = (char*)ctx->d_sky.p;
   double* buf_e[2] = {(double*)base, (double*)(base + tri)};
@@ -597,6 +713,33 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   int which = 0;
   bool stalled = false;
   FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
+  int64_t pre_min = (int64_t)1 << 20;
+  if (const char* ev = getenv("FFB_SKYLINE_PREFILTER_MIN")) pre_min = atoll(ev);      // test hook: small sets through the pre-filter
+  if (!d_occ && n >= pre_min) {
+    // large two-objective sets: the streaming pre-filter first (see above); when its survivors do not fit the work
+    // buffer (a set that is mostly front) the levels below start from the whole set as before
+    PreArgs pa = {};
+    pa.e = d_e; pa.t = d_t; pa.id = d_id; pa.n = n;
+    pa.gmin = (unsigned long long*)(base + 2 * tri + 256); pa.range = (double*)(base + 2 * tri + 256 + (size_t)kPreBuckets * 8);
+    pa.out_e = buf_e[0]; pa.out_t = buf_t[0]; pa.out_id = buf_id[0]; pa.out_cap = work_cap;
+    pa.out_count = d_count + 3; pa.overflow = d_status + 1;
+    unsigned ctas = (unsigned)ctx->sm_count * 4;
+    if ((int64_t)ctas * kPreThreads > n) ctas = (unsigned)((n + kPreThreads - 1) / kPreThreads);
+    FFB_LAUNCH(pre_range_kernel, 1, 1024, 0, stream, pa);
+    FFB_LAUNCH(pre_min_kernel, ctas, kPreThreads, 0, stream, pa);
+    FFB_LAUNCH(pre_prefix_kernel, 1, 1024, 0, stream, pa);
+    FFB_LAUNCH(pre_filter_kernel, ctas, kPreThreads, 0, stream, pa);
+    rc = ffb_check_launch(ctx, "skyline pre-filter");
+    if (rc) return rc;
+    unsigned long long h_kept = 0; uint32_t h_over = 0;
+    FFB_CUDA(ctx, cudaMemcpyAsync(&h_kept, pa.out_count, sizeof(h_kept), cudaMemcpyDeviceToHost, stream));
+    FFB_CUDA(ctx, cudaMemcpyAsync(&h_over, pa.overflow, sizeof(h_over), cudaMemcpyDeviceToHost, stream));
+    FFB_CUDA(ctx, cudaStreamSynchronize(stream));
+    if (!h_over && (int64_t)h_kept <= work_cap) {
+      cur_e = buf_e[0]; cur_t = buf_t[0]; cur_id = buf_id[0]; cur_n = (int64_t)h_kept; which = 1;
+    }
+    FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
+  }
   for (int level = 0; level < 64; ++level) {
     // normally the last level is one resident chunk; a set that stopped shrinking (its front is
     // larger than a chunk, e.g. heavy ties) is finished by one CTA streaming from L2 with the

@@ -83,6 +83,33 @@ def test_large_set_hierarchical(backend, kind):
     assert ids2.cpu().numpy().tolist() == want
 
 
+@pytest.mark.parametrize("kind", ["uniform", "tied", "anticorrelated", "specials", "constant_e"])
+def test_streaming_prefilter_keeps_the_front(backend, kind, monkeypatch):
+    """Sets of 2^20 candidates and more first go through the two-pass bucket pre-filter of ffb_skyline; the
+    threshold is lowered here so that the CPU suite covers it too: same front, same order, same t_peak,
+    with ties, NaNs, infinities and a degenerate e range."""
+    monkeypatch.setenv("FFB_SKYLINE_PREFILTER_MIN", "1000")
+    n = 20_000 if backend == "emul" else 3_000_000
+    if kind == "specials":
+        e, t = synth.candidate_cloud(seed=8, n=n, kind="uniform")
+        rng = np.random.default_rng(8)
+        e[rng.integers(0, n, 50)] = np.inf
+        t[rng.integers(0, n, 50)] = np.inf
+        e[rng.integers(0, n, 20)] = -1e300                          # far below the sampled range
+        e[:3] = 1e300
+    elif kind == "constant_e":
+        e, t = np.full(n, 2.5), np.random.default_rng(3).integers(0, 50, n).astype(np.float64)
+    else:
+        e, t = synth.candidate_cloud(seed=6, n=n, kind=kind)
+    cap = 1 << 15
+    rho = 0.9 if kind == "uniform" else 0.0
+    ids, fe, ft, tpk = engine.skyline(_dev(e), _dev(t), rho=rho, cap_front=cap)
+    want, wtp = orc.pareto_indices(e, t, rho=rho)
+    assert ids.cpu().numpy().tolist() == want
+    assert np.array_equal(fe.cpu().numpy(), e[want]) and np.array_equal(ft.cpu().numpy(), t[want])
+    assert tpk == wtp
+
+
 @pytest.mark.parametrize("levels,rho", [(1, 0.0), (4, 0.0), (9, 0.9), (64, 0.0)])
 def test_three_objective_groups_match_oracle(backend, levels, rho):
     """Extension (occupancy as a third objective): groups against the O(n^2) definition in the oracle;
