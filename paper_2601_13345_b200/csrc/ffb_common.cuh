@@ -43,6 +43,7 @@ struct FfbContext {
   FfbBuf d_lex;        // lexer scratch
   FfbBuf d_flow;       // dataflow scratch
   FfbBuf d_explore;    // fused explore: tie ranks + counter
+  FfbBuf d_bigfront;   // sort-based finish of large fronts (ffb_bigfront.cu)
   std::vector<uint16_t> explore_shadow;   // host copy of the tie-order table d_explore holds
   void* explore_shadow_dev = nullptr;
   void* h_stage = nullptr;   // pinned staging for table uploads
@@ -59,6 +60,10 @@ int32_t ffb_fail(FfbContext* ctx, int32_t code, const char* fmt, ...);
 int32_t ffb_reserve(FfbContext* ctx, FfbBuf* b, size_t bytes);
 int32_t ffb_stage_reserve(FfbContext* ctx, size_t bytes);   // waits until earlier uploads drained
 int32_t ffb_check_launch(FfbContext* ctx, const char* what);
+// ffb_bigfront.cu: exact front of a set whose front does not fit one CTA (device-wide sort); synchronises
+int32_t ffb_big_front(FfbContext* ctx, const double* d_e, const double* d_t, const uint64_t* d_id, int64_t n, double rho,
+                      uint64_t* d_front_id, double* d_front_e, double* d_front_t, int64_t cap_front,
+                      int64_t* h_front_n, double* h_tpeak, cudaStream_t stream);
 
 #define FFB_CUDA(ctx, expr)                                                        \
   do {                                                                             \

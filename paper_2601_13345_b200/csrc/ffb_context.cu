@@ -83,7 +83,7 @@ int32_t ffb_destroy(FfbContext* ctx) {
   if (!ctx) return FFB_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  FfbBuf* bufs[] = {&ctx->d_tables, &ctx->d_kstab, &ctx->d_sky, &ctx->d_lex, &ctx->d_flow, &ctx->d_explore};
+  FfbBuf* bufs[] = {&ctx->d_tables, &ctx->d_kstab, &ctx->d_sky, &ctx->d_lex, &ctx->d_flow, &ctx->d_explore, &ctx->d_bigfront};
   for (FfbBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);

@@ -505,17 +505,19 @@ Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie, bool h
 }
 
 // ---- streaming pre-filter of one huge candidate set (two objectives) --------------------------------
-// Two coalesced passes over (e, t) take the set from n to roughly n / kPreBuckets + the neighbourhood of the
-// front before any sorting starts: pass 1 leaves min t per e-bucket (any monotone bucketing of e is valid, the
+// Two coalesced passes over (e, t) (the first one over a 1/16 sample when the set is large) take the set from n to
+// roughly n / kPreBuckets + the neighbourhood of the front before any sorting starts: pass 1 leaves min t per e-bucket (any monotone bucketing of e is valid, the
 // range comes from a sample and out-of-range values clamp to the edge buckets), an exclusive prefix-min over
 // the buckets follows, pass 2 keeps a candidate unless a STRICTLY lower bucket holds a strictly smaller t -
 // i.e. unless it is provably dominated (explorer.py:122-140: drop iff some j has e_j < e_i and t_j < t_i).
 // NaNs neither dominate nor get dropped.  Survivors are compacted with their ids.
 constexpr int kPreBuckets = 4096;
 constexpr int kPreThreads = 512;
+constexpr int kPreRun = 4096;                                 // candidates per sampled run of pass 1
 struct PreArgs {
   const double* e; const double* t; const uint64_t* id;
   int64_t n;
+  int64_t sample;                   // pass 1 reads every sample-th run of kPreRun candidates (1: all)
   double* range;                    // {lo, scale}
   unsigned long long* gmin;         // [kPreBuckets] min t per bucket, later the exclusive prefix-min
   double* out_e; double* out_t; uint64_t* out_id;
@@ -556,7 +558,11 @@ __global__ void __launch_bounds__(kPreThreads) pre_min_kernel(PreArgs a) {
   for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads) s_min[b] = ~0ull;
   __syncthreads();
   const double lo = a.range[0], scale = a.range[1];
-  for (int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kPreThreads) {
+  // every `sample`-th run of kPreRun candidates: a minimum over a SUBSET is still a valid certificate (the pass-2
+  // test names an existing dominator), so large sets pay one full pass instead of two
+  const int64_t n_s = a.sample > 1 ? (a.n / ((int64_t)kPreRun * a.sample)) * kPreRun : a.n;
+  for (int64_t j = (int64_t)blockIdx.x * kPreThreads + threadIdx.x; j < n_s; j += (int64_t)gridDim.x * kPreThreads) {
+    const int64_t i = a.sample > 1 ? (j / kPreRun) * ((int64_t)kPreRun * a.sample) + (j % kPreRun) : j;
     const double ev = a.e[i], tv = a.t[i];
     if (ev != ev || tv != tv) continue;
     const int b = pre_bucket(ev, lo, scale);
@@ -720,6 +726,7 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
     // buffer (a set that is mostly front) the levels below start from the whole set as before
     PreArgs pa = {};
     pa.e = d_e; pa.t = d_t; pa.id = d_id; pa.n = n;
+    pa.sample = n >= ((int64_t)1 << 26) ? 16 : 1;
     pa.gmin = (unsigned long long*)(base + 2 * tri + 256); pa.range = (double*)(base + 2 * tri + 256 + (size_t)kPreBuckets * 8);
     pa.out_e = buf_e[0]; pa.out_t = buf_t[0]; pa.out_id = buf_id[0]; pa.out_cap = work_cap;
     pa.out_count = d_count + 3; pa.overflow = d_status + 1;
@@ -770,9 +777,14 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
     FFB_CUDA(ctx, cudaMemcpyAsync(&h_count, a.out_count, sizeof(h_count), cudaMemcpyDeviceToHost, stream));
     FFB_CUDA(ctx, cudaMemcpyAsync(&h_status, d_status, sizeof(h_status), cudaMemcpyDeviceToHost, stream));
     FFB_CUDA(ctx, cudaStreamSynchronize(stream));
-    if (h_status & (1u << FFB_E_CAPACITY))
+    if (h_status & (1u << FFB_E_CAPACITY)) {
+      // the chunk fronts (or the final group's front) outgrew their buffer: a set that is mostly front.  Two
+      // objectives finish with the device-wide sort over what this level STARTED from (ffb_bigfront.cu).
+      if (!d_occ && cur_n < ((int64_t)1 << 32))
+        return ffb_big_front(ctx, cur_e, cur_t, cur_id, cur_n, rho, d_front_id, d_front_e, d_front_t, cap_front, h_front_n, h_tpeak, stream);
       return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: front exceeds capacity at level %d (%llu candidates kept of %lld)",
                       level, h_count, (long long)cur_n);
+    }
     if (last) {
       *h_front_n = (int64_t)h_count;
       if (h_tpeak) {
@@ -784,9 +796,15 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
       return FFB_OK;
     }
     if ((int64_t)h_count * 4 > cur_n * 3) {
-      if ((int64_t)h_count > (1 << 20))
-        return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: candidate set does not reduce (%llu of %lld on chunk fronts)",
-                        h_count, (long long)cur_n);
+      // the set stopped shrinking: its front is larger than a chunk (ties).  Small ones are finished by one CTA
+      // streaming from L2; larger ones by the device-wide sort (two objectives)
+      if ((int64_t)h_count > 8192) {
+        if (d_occ || (int64_t)h_count >= ((int64_t)1 << 32))
+          return ffb_fail(ctx, FFB_E_CAPACITY, "ffb_skyline: candidate set does not reduce (%llu of %lld on chunk fronts)",
+                          h_count, (long long)cur_n);
+        return ffb_big_front(ctx, buf_e[which], buf_t[which], buf_id[which], (int64_t)h_count, rho, d_front_id, d_front_e, d_front_t,
+                             cap_front, h_front_n, h_tpeak, stream);
+      }
       stalled = true;
     }
     cur_e = buf_e[which]; cur_t = buf_t[which]; cur_id = buf_id[which];

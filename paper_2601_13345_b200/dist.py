@@ -75,7 +75,8 @@ def sharded_skyline(e: torch.Tensor, t: torch.Tensor, first_id: int, *, rho: flo
     """Front of a candidate set whose shard [first_id, first_id + len(e)) lives on this rank
     (two objectives, or three with ``occ``)."""
     rt = rt or native.get_runtime()
-    ids = torch.arange(first_id, first_id + e.numel(), dtype=torch.int64, device=rt.device)
-    lid, le, lt, _ = engine.skyline(e, t, ids=ids, rho=0.0, cap_front=cap_front, rt=rt, occ=occ)   # floor only at the end
-    locc = occ[lid - first_id].contiguous() if occ is not None else None
+    # ids are positions in the shard (no id array for 10^9 candidates); the global id is first_id + position
+    lpos, le, lt, _ = engine.skyline(e, t, rho=0.0, cap_front=cap_front, rt=rt, occ=occ)   # floor only at the end
+    locc = occ[lpos].contiguous() if occ is not None else None
+    lid = lpos + first_id
     return merge_fronts(lid, le, lt, rho=rho, cap_front=cap_front, group=group, rt=rt, occ=locc)

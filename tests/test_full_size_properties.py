@@ -125,6 +125,36 @@ def test_front_of_1e9_candidates(gpu_only, kind):
     assert torch.equal(ids2, ids) and torch.equal(fe2, fe) and torch.equal(ft2, ft)
 
 
+def test_tied_front_of_1e9_candidates(gpu_only):
+    """configs[4] with the clustered / tied distribution of pkg/tests/test_acceptance.py:114-115 at 10^9: every
+    candidate with the lowest e or the lowest t is on the front (5% of the set, all exact ties), far beyond what
+    one CTA can sort - the streaming pre-filter leaves exactly those, the device-wide sort orders them."""
+    rt = gpu_only
+    n = 1_000_000_000
+    g = torch.Generator(device=rt.device).manual_seed(11)
+    e = torch.empty(n, dtype=torch.float64, device=rt.device)
+    t = torch.empty(n, dtype=torch.float64, device=rt.device)
+    step = 1 << 27
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        e[lo:hi] = torch.randint(0, 40, (hi - lo,), generator=g, device=rt.device).to(torch.float64) / 4.0
+        t[lo:hi] = torch.randint(0, 40, (hi - lo,), generator=g, device=rt.device).to(torch.float64) / 4.0
+    on_front = (e == 0.0) | (t == 0.0)
+    m = int(on_front.sum().item())
+    assert m > 40_000_000
+    ids, fe, ft, tpk = engine.skyline(e, t, rho=0.0, cap_front=m + 16, rt=rt)
+    torch.cuda.synchronize()
+    assert ids.numel() == m and tpk == 0.0
+    assert bool(on_front[ids].all())
+    assert bool((e[ids] == fe).all()) and bool((t[ids] == ft).all())
+    # reference order: (e, t, id) ascending
+    same_e = fe[1:] == fe[:-1]
+    assert bool((fe[1:] >= fe[:-1]).all())
+    assert bool((ft[1:][same_e] >= ft[:-1][same_e]).all())
+    same_et = same_e & (ft[1:] == ft[:-1])
+    assert bool((ids[1:][same_et] > ids[:-1][same_et]).all())
+
+
 def test_three_objective_front_of_1e9_candidates(gpu_only):
     """configs[4], "+occupancy" (extension): 10^9 candidates with 8 occupancy levels.  The 2-objective front is
     a subset of the 3-objective one (3-objective dominance implies 2-objective dominance), no front member is

@@ -101,13 +101,34 @@ def test_streaming_prefilter_keeps_the_front(backend, kind, monkeypatch):
         e, t = np.full(n, 2.5), np.random.default_rng(3).integers(0, 50, n).astype(np.float64)
     else:
         e, t = synth.candidate_cloud(seed=6, n=n, kind=kind)
-    cap = 1 << 15
     rho = 0.9 if kind == "uniform" else 0.0
-    ids, fe, ft, tpk = engine.skyline(_dev(e), _dev(t), rho=rho, cap_front=cap)
     want, wtp = orc.pareto_indices(e, t, rho=rho)
+    ids, fe, ft, tpk = engine.skyline(_dev(e), _dev(t), rho=rho, cap_front=max(1 << 15, len(want) + 8))
     assert ids.cpu().numpy().tolist() == want
     assert np.array_equal(fe.cpu().numpy(), e[want]) and np.array_equal(ft.cpu().numpy(), t[want])
     assert tpk == wtp
+
+
+@pytest.mark.parametrize("kind", ["all_on_front", "tied", "tied_floor"])
+def test_front_larger_than_one_cta(backend, kind):
+    """Fronts that hold a constant fraction of the set (ties, anti-correlated clouds) are finished by the
+    device-wide sort of ffb_bigfront.cu: membership, reference order (e, t, id) and t_peak as the oracle."""
+    n = 30_000 if backend == "emul" else 2_000_000
+    rng = np.random.default_rng(12)
+    if kind == "all_on_front":
+        e = np.arange(n, dtype=np.float64) // 3                      # triples of equal e ...
+        t = (n - np.arange(n, dtype=np.float64)) // 3 + rng.integers(0, 2, n)      # ... t falls as e grows: nearly all stay
+    else:
+        e, t = synth.candidate_cloud(seed=13, n=n, kind="tied")     # pkg/tests/test_acceptance.py:114-115 distribution
+    rho = 0.5 if kind == "tied_floor" else 0.0
+    want, wtp = orc.pareto_indices(e, t, rho=rho)
+    assert len(want) > (65535 if backend == "gpu" and rho == 0.0 else (8192 if kind == "all_on_front" else 500))
+    ids, fe, ft, tpk = engine.skyline(_dev(e), _dev(t), rho=rho, cap_front=len(want) + 5)
+    assert ids.cpu().numpy().tolist() == want
+    assert np.array_equal(fe.cpu().numpy(), e[want]) and np.array_equal(ft.cpu().numpy(), t[want])
+    assert tpk == wtp
+    with pytest.raises(CapacityExceeded):
+        engine.skyline(_dev(e), _dev(t), rho=rho, cap_front=len(want) - 1)
 
 
 @pytest.mark.parametrize("levels,rho", [(1, 0.0), (4, 0.0), (9, 0.9), (64, 0.0)])
