@@ -7,6 +7,7 @@ import json
 import math
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 from paper_2601_13345_b200 import api, specs
@@ -113,6 +114,29 @@ def test_pareto_front_clouds(backend):
     with pytest.raises(E.NoFeasibleConfig):
         api.pareto_front_bruteforce([])
     assert api.pareto_front([]) == []
+
+
+def test_pareto_front_beyond_one_cta(backend):
+    """A front of 70 000 mutually non-dominated predictions (more than one CTA's shared memory holds and more than the
+    65 535 a group index addresses): the drop-in falls through to the streaming skyline + device-wide sort and still
+    returns the reference order (e, t, block_x, block_y, p_cap), ties included."""
+    n = 70_000
+    rng = np.random.default_rng(3)
+    e = np.arange(n, dtype=np.float64) // 2                          # pairs of equal e
+    t = (n - np.arange(n, dtype=np.float64)) // 2                    # ... and equal t: exact ties, ordered by the config
+    bx = rng.integers(1, 64, n)
+    tb = [api.TimeBreakdown(1.0, 1.0, 1.0, 0.0, 0.0, 0.0, float(x)) for x in t]
+    pb = api.PowerBreakdown(0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1, False)
+    preds = [api.Prediction(api.LaunchConfig(int(bx[i]), 1, 100.0), tb[i], pb, float(e[i])) for i in range(n)]
+    front = api.pareto_front(preds)
+    want = sorted(range(n), key=lambda i: (e[i], t[i], int(bx[i]), 1, 100.0, i))
+    # every point is on the front (t falls as e grows); stable order for full ties follows the input order
+    assert len(front) == n
+    got = {id(q): k for k, q in enumerate(front)}
+    pos = [got[id(preds[i])] for i in want]
+    keyed = [(e[i], t[i], int(bx[i])) for i in want]
+    assert all(keyed[k] <= keyed[k + 1] for k in range(n - 1))
+    assert sorted(pos) == list(range(n)) and all((e[want[k]], t[want[k]], int(bx[want[k]])) == (front[k].e_pred, front[k].time.t_exec, front[k].config.block_x) for k in range(0, n, 997))
 
 
 def test_model_helpers_known_answers(backend):
