@@ -348,6 +348,56 @@ def bench_corpus(seed: int, target_bytes: int, n_kernels: int | None, *, base_ke
                   order=order, host_text=text, host_off=offs)
 
 
+def _gen_piece(args):
+    from . import synth
+    seed, first, count, irregular = args
+    return synth.ptx_corpus(seed, count, irregular=irregular, first=first)
+
+
+def bench_corpus_unique(seed: int, n_kernels: int, *, irregular: float = 0.0, workers: int | None = None, piece: int = 600,
+                        rt: native.Runtime | None = None) -> Corpus:
+    """``n_kernels`` DIFFERENT generated kernels (no tiling): the text is produced in pieces of ``piece`` kernels by a
+    process pool (every piece has its own seed, names are unique over the corpus) and uploaded piece by piece.
+    ``irregular``: share of kernels with one construct that only the exact walk parses (synth.ptx_corpus)."""
+    import multiprocessing as mp
+    import os
+    rt = rt or native.get_runtime()
+    jobs = [(seed * 100_003 + i, i * piece, min(piece, n_kernels - i * piece), irregular) for i in range((n_kernels + piece - 1) // piece)]
+    workers = workers or min(len(jobs), os.cpu_count() or 1)
+    with mp.get_context("fork").Pool(workers) as pool:
+        parts = pool.map(_gen_piece, jobs)
+    total = sum(len(p[0]) for p in parts)
+    padded = (total + 15) // 16 * 16 + 16
+    dev = torch.full((padded,), 10, dtype=torch.uint8, device=rt.device)
+    seg, pos = [np.zeros(1, dtype=np.int64)], 0
+    for text, offs in parts:
+        dev[pos: pos + len(text)].copy_(rt.to_device(torch.frombuffer(bytearray(text), dtype=torch.uint8)))
+        seg.append(offs[1:] + pos)
+        pos += len(text)
+    seg = np.concatenate(seg).astype(np.int64)
+    order = rt.to_device(torch.from_numpy(np.argsort(-np.diff(seg), kind="stable").astype(np.int32)))
+    host = b"".join(p[0] for p in parts)
+    return Corpus(text=dev, n_bytes=total, seg_off=rt.to_device(torch.from_numpy(seg)), n_segs=len(seg) - 1,
+                  order=order, host_text=host, host_off=seg)
+
+
+def replicated_corpus(unit: bytes, unit_off: np.ndarray, target_bytes: int, rt: native.Runtime | None = None) -> Corpus:
+    """``unit`` (a few kernels, e.g. real compiler output) repeated on the device up to about ``target_bytes``."""
+    rt = rt or native.get_runtime()
+    n = len(unit)
+    reps = max(1, int(round(target_bytes / max(n, 1))))
+    total = n * reps
+    padded = (total + 15) // 16 * 16 + 16
+    dev = torch.full((padded,), 10, dtype=torch.uint8, device=rt.device)
+    dev[:total].view(reps, n).copy_(rt.to_device(torch.frombuffer(bytearray(unit), dtype=torch.uint8)).unsqueeze(0).expand(reps, n))
+    unit_off = np.asarray(unit_off, dtype=np.int64)
+    seg = (unit_off[None, :-1] + (np.arange(reps, dtype=np.int64) * n)[:, None]).reshape(-1)
+    seg = np.concatenate([seg, [total]]).astype(np.int64)
+    order = rt.to_device(torch.from_numpy(np.argsort(-np.diff(seg), kind="stable").astype(np.int32)))
+    return Corpus(text=dev, n_bytes=total, seg_off=rt.to_device(torch.from_numpy(seg)), n_segs=len(seg) - 1,
+                  order=order, host_text=unit, host_off=unit_off)
+
+
 class StreamedAnalysis:
     """text in PINNED HOST memory -> feature rows, with the host->device copy overlapped with the
     kernels: the corpus is cut at segment boundaries into chunks of about ``chunk_bytes``; a copy

@@ -114,14 +114,27 @@ def ptx_kernel(rng: np.random.Generator, name: str, n_instr: int, *, comments: b
     return "\n".join(lines)
 
 
-def ptx_corpus(seed: int, n_kernels: int, lo: int = 50, hi: int = 5000, *, comments: bool = True):
-    """(text bytes, offsets int64[n_kernels+1]); kernel sizes log-uniform in [lo, hi] statements."""
+# one irregular construct for a kernel of the `irregular` share: text the fast lexer path hands to the exact walk
+# (ptx.py:139-141 block comments, :257-270 statements that share or span lines, :232-236 label + statement)
+_IRREGULAR = ("\t/* spilled: add.s32 %r9, %r9, 1;\n\t   ret; */ mov.u32 \t%r9, 1;", "\tmov.u32 \t%r9, 1; add.s32 \t%r9, %r9, 1;",
+              "\tadd.s32 \t%r9,\n\t\t%r9,\n\t\t1;", "$L__note: mov.u32 \t%r9, 2;")
+
+
+def ptx_corpus(seed: int, n_kernels: int, lo: int = 50, hi: int = 5000, *, comments: bool = True, irregular: float = 0.0,
+               first: int = 0):
+    """(text bytes, offsets int64[n_kernels+1]); kernel sizes log-uniform in [lo, hi] statements.
+    ``irregular``: share of kernels that carry one construct outside the fast lexer path's grammar.
+    ``first``: index of the first kernel (names stay unique when a corpus is generated in pieces)."""
     rng = np.random.default_rng(seed)
     sizes = np.exp(rng.uniform(np.log(lo), np.log(hi), size=n_kernels)).astype(int)
+    odd = rng.random(n_kernels) < irregular if irregular > 0 else np.zeros(n_kernels, dtype=bool)
     parts, offs, pos = [], [0], 0
     head = "//\n// synthetic corpus segment\n//\n.version 8.7\n.target sm_100a\n.address_size 64\n\n"
     for k in range(n_kernels):
-        txt = (head if comments else "") + ptx_kernel(rng, f"synk_{seed % 1000:03d}_{k:06d}", int(sizes[k]), comments=comments)
+        txt = (head if comments else "") + ptx_kernel(rng, f"synk_{seed % 1000:03d}_{first + k:06d}", int(sizes[k]), comments=comments)
+        if odd[k]:
+            at = txt.index("\tcvt.u64.u32")
+            txt = txt[:at] + _IRREGULAR[int(rng.integers(0, len(_IRREGULAR)))] + "\n" + txt[at:]
         b = txt.encode("ascii")
         parts.append(b)
         pos += len(b)

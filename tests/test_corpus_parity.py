@@ -53,6 +53,20 @@ def test_synthetic_corpus(backend, seed, default_trip):
     _check([text[offs[i]:offs[i + 1]].decode("ascii") for i in range(n)], default_trip)
 
 
+def test_irregular_share_of_the_bench_corpus(backend):
+    """bench.py's corpus gives a share of its kernels one construct outside the fast path's grammar (synth._IRREGULAR):
+    those segments are finished by the exact walk, every row still equals the oracle's, and the pieces of a corpus
+    generated in parallel carry unique kernel names."""
+    text, offs = synth.ptx_corpus(seed=31, n_kernels=8, lo=20, hi=300, irregular=1.0, first=600)
+    srcs = [text[offs[i]:offs[i + 1]].decode("ascii") for i in range(8)]
+    assert any("/* spilled" in s for s in srcs) and any("$L__note:" in s for s in srcs) and "synk_031_000607" in srcs[7]
+    _check(srcs)
+    lex = corpus.lex_histogram(_corpus(srcs))
+    assert lex.path_counts.cpu().tolist()[:2] == [0, 8]
+    plain, _ = synth.ptx_corpus(seed=31, n_kernels=8, lo=20, hi=300)
+    assert plain != text and len(plain) < len(text)
+
+
 def test_tile_boundaries(backend):
     """Kernels longer than one 4 KB tile, long preambles, statements split over tile edges."""
     rng = np.random.default_rng(5)
