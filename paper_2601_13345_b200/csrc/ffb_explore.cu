@@ -43,6 +43,7 @@ constexpr int kXThreads = 512;
 constexpr int kXWarps = kXThreads / 32;
 constexpr int kDigits = 64;                    // radix of the final stable sort (6 bits per pass)
 constexpr unsigned kXAll = 0xffffffffu;
+constexpr int kMaxClassA = 96;                 // (threads, regs) classes kept on chip; shape tables with more fall back to eval_unit
 
 struct ExploreArgs {
   const double* feat;
@@ -189,6 +190,8 @@ __global__ void __launch_bounds__(kXThreads, 2)
 explore_groups_kernel(ExploreArgs a) {
   FFB_DYN_SMEM(smem_raw);
   __shared__ double s_kr[kKsWidth];
+  __shared__ double s_ca[kMaxClassA * kClassAWidth];     // factored model: rows per (threads, regs) class ...
+  __shared__ double s_cb[33 * kClassBWidth];             // ... and per clipped block_x
   __shared__ double s_part[kXThreads / 32 + 1];
   __shared__ uint32_t s_pc[kXThreads / 32];
   __shared__ unsigned long long s_pm[kXThreads / 32];
@@ -231,20 +234,41 @@ explore_groups_kernel(ExploreArgs a) {
   // ---- 1. the model: one thread per shape, cap axis innermost ----
   double tmin = INFINITY;
   const double2* ct = reinterpret_cast<const double2*>(a.tb.cap_tab + (size_t)s * C * 4);
+  // the class rows first (32 + 32 for the reference's 464 shapes), then two divides per shape; kernels whose row
+  // carries override columns, and shape tables with too many classes, evaluate every shape in full
+  const bool classes = a.tb.n_a > 0 && a.tb.n_a <= kMaxClassA && f[FFB_F_OVR] == 0.0;
+  if (classes) {
+    for (int i = tid; i < a.tb.n_a + a.tb.n_b; i += kXThreads) {
+      if (i < a.tb.n_a) eval_class_a(f, sp, sd, s_kr, a.tb.a_rep[2 * i], a.tb.a_rep[2 * i + 1], shared_dyn, total_blocks, s_ca + i * kClassAWidth);
+      else eval_class_b(f, sp, sd, a.tb.b_rep[i - a.tb.n_a], s_cb + (i - a.tb.n_a) * kClassBWidth);
+    }
+    __syncthreads();
+  }
+  const double p_static = sp[FFB_S_P_STATIC], e_over = sp[FFB_S_E_OVERHEAD];
   for (int j = tid; j < J; j += kXThreads) {
-    Unit u;
-    eval_unit(f, sp, sd, s_kr, a.tb.shape + 4 * j, a.tb.shape_log[j], shared_dyn, total_blocks, 0, u);
+    double t_exec, p_pre;
+    bool valid;
+    if (classes) {
+      const int32_t cls = a.tb.shape_cls[j];
+      const double* ca = s_ca + (cls & 0xffff) * kClassAWidth;
+      eval_shape(sp, s_kr, ca, s_cb + (cls >> 16) * kClassBWidth, a.tb.shape_log[j], &t_exec, &p_pre);
+      valid = ca[CA_VALID] != 0.0;
+    } else {
+      Unit u;
+      eval_unit(f, sp, sd, s_kr, a.tb.shape + 4 * j, a.tb.shape_log[j], shared_dyn, total_blocks, 0, u);
+      t_exec = u.t_exec; p_pre = u.p_pre; valid = u.valid;
+    }
     bool any_ok = false;
     for (int c = 0; c < C; ++c) {
       const double2 sc_cap = ct[2 * c], room_ok = ct[2 * c + 1];
       double p_dyn;
       bool limited;
-      const double e = eval_cap(u.t_exec, u.p_pre, u.p_static, u.e_over, sc_cap.x, sc_cap.y, room_ok.x, &p_dyn, &limited);
-      const bool ok = u.valid && room_ok.y != 0.0;
+      const double e = eval_cap(t_exec, p_pre, p_static, e_over, sc_cap.x, sc_cap.y, room_ok.x, &p_dyn, &limited);
+      const bool ok = valid && room_ok.y != 0.0;
       s_e[j * C + c] = ok ? e + 0.0 : INFINITY;            // (+ 0.0: -0.0 and 0.0 are one key)
       any_ok = any_ok || ok;
     }
-    const double tj = any_ok ? u.t_exec + 0.0 : INFINITY;
+    const double tj = any_ok ? t_exec + 0.0 : INFINITY;
     s_t[j] = tj;
     tmin = tj < tmin ? tj : tmin;
   }

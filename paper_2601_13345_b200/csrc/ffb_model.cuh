@@ -30,6 +30,11 @@ struct Tables {
   const double* cap_tab;   // [S, C, 4] {scale, cap, max(0, cap - p_static), ok}: the cap axis in one 32-byte row
   const double* psm;       // [S, psm_n]
   int psm_n;
+  // shape classes (host-built): shape j -> class A row (threads, regs) | class B row (min(block_x, 32)) << 16
+  const int32_t* shape_cls;   // [J]
+  const int32_t* a_rep;       // [n_a, 2] {threads, regs}
+  const int32_t* b_rep;       // [n_b]    block_x clipped to 32
+  int n_a, n_b;
 };
 
 // ---- per (kernel, spec) hoisting: time_model.py:47-64 (_issue_window), :40-44 (cwp),
@@ -151,6 +156,82 @@ FFB_D void eval_unit(const double* f, const double* sp, const double* sd, const 
   u.err = err;
   u.mwp = mwp; u.bw_eff = bw_eff; u.t_mem = t_mem; u.t_comp = t_comp; u.t_sync = t_sync; u.p_units = p_units; u.p_shape = p_shape;
   u.p_mem = p_mem; u.p_sm = p_sm; u.ci = ci; u.eta = eta; u.waves = waves; u.warps = warps;
+}
+
+// ---- the same chain, factored by what each part depends on --------------------------------------------
+// Of a unit's cap-independent chain only p_shape reads |ln(bx / by)|; occupancy, waves, t_comp, t_sync and
+// p_units depend on (threads, regs) alone, eta / bandwidth / p_mem on min(block_x, 32) alone.  The 464 shapes of
+// the reference's search space have 32 distinct thread counts and 32 distinct clipped block_x values, so a
+// (kernel, spec) group evaluates 32 + 32 class rows (about ten fp64 divides each) and two divides per shape
+// instead of ten per shape.  Every expression keeps the operand order of eval_unit: same bits.
+// (Rows with override columns - the single-point drop-ins - stay on eval_unit.)
+constexpr int kClassAWidth = 8, kClassBWidth = 4;
+enum { CA_MB = 0, CA_T_COMP, CA_T_SYNC, CA_P_UNITS, CA_BPS, CA_VALID, CA_WAVES, CA_WARPS };
+enum { CB_DEN_MEM = 0, CB_P_MEM, CB_ETA, CB_BW_EFF };
+
+FFB_D void eval_class_a(const double* f, const double* sp, const double* sd, const double* kr, int64_t threads, int64_t regs,
+                        int64_t shared_dyn, int64_t total_blocks, double* o) {
+  const int64_t max_threads = (int64_t)sp[FFB_S_MAX_THREADS];
+  const int64_t max_warps = (int64_t)sp[FFB_S_MAX_WARPS];
+  const bool shape_ok = threads >= 32 && threads <= max_threads && (threads % 32) == 0;
+  const int64_t warps = shape_ok ? threads / 32 : 1;
+  bool fits = warps <= max_warps;
+  if (shared_dyn > 0) fits = fits && shared_dyn <= (int64_t)sp[FFB_S_MAX_SHARED];
+  const double wf = (double)warps;
+  double bps = sp[FFB_S_MAX_WARPS] / wf;                            // features.py:112
+  bps = py_min(bps, kr[KS_SHARED_LIMIT]);                           // features.py:114
+  const double regs_per_sm = sp[FFB_S_REGS_PER_SM];
+  if (regs_per_sm > 0.0 && regs > 0) {                              // extension: oracle.occupancy_ext
+    const double reg_limit = regs_per_sm / (double)(regs * threads);
+    bps = py_min(bps, reg_limit);
+    fits = fits && reg_limit >= 1.0;
+  }
+  const double resident = py_min(bps * wf, (double)max_warps);      // time_model.py:78
+  const double lanes = (sp[FFB_S_SM_COUNT] * resident) * 32.0;
+  const double tthreads = (double)(total_blocks * warps) * 32.0;
+  const double waves = py_max(1.0, tthreads / lanes);
+  const double nc = kr[KS_N_COMP] * waves;
+  const double wps = py_min(wf * bps, (double)max_warps);           // power_model.py:124
+  double p_units = 0.0;
+  const uint32_t skip = (uint32_t)sd[SD_SKIPMASK];
+#pragma unroll
+  for (int x = 0; x < 5; ++x) {
+    if (skip & (1u << x)) continue;
+    const double cnt = (x == 4) ? f[FFB_F_N_MEM] : f[FFB_F_FP32 + x];
+    const double rate = (cnt * wps) / sd[SD_RATIO0 + x];
+    p_units = p_units + sp[FFB_S_BETA0 + x] * rate;
+  }
+  o[CA_MB] = f[FFB_F_MEM_BYTES] * waves;
+  o[CA_T_COMP] = (nc > 0.0) ? nc / kr[KS_DENOM_COMP] : 0.0;
+  o[CA_T_SYNC] = (f[FFB_F_N_SYNC] * waves) * sp[FFB_S_T_BARRIER];
+  o[CA_P_UNITS] = p_units;
+  o[CA_BPS] = bps;
+  o[CA_VALID] = (shape_ok && fits) ? 1.0 : 0.0;
+  o[CA_WAVES] = waves;
+  o[CA_WARPS] = wf;
+}
+FFB_D void eval_class_b(const double* f, const double* sp, const double* sd, int64_t bx, double* o) {
+  const double eta = py_min(1.0, (double)bx / 32.0) * f[FFB_F_ALIGNED];            // features.py:59
+  const double bw_eff = sp[FFB_S_BW_MAX] * py_max(eta, sd[SD_FLOOR]);
+  o[CB_DEN_MEM] = sd[SD_MWP] * bw_eff;
+  o[CB_P_MEM] = sp[FFB_S_P_MEM_BASE] * (1.0 + sp[FFB_S_LAMBDA] * (1.0 - eta));
+  o[CB_ETA] = eta;
+  o[CB_BW_EFF] = bw_eff;
+}
+// one shape from its two class rows: t_exec and the cap-independent dynamic power
+FFB_D void eval_shape(const double* sp, const double* kr, const double* ca, const double* cb, double shape_log, double* t_exec_out, double* p_pre_out) {
+  const double mb = ca[CA_MB];
+  const double t_mem = (mb > 0.0) ? mb / cb[CB_DEN_MEM] : 0.0;
+  const double t_exec = ((sp[FFB_S_W_MEM] * t_mem + sp[FFB_S_W_COMP] * ca[CA_T_COMP]) + sp[FFB_S_W_SYNC] * ca[CA_T_SYNC]) + sp[FFB_S_T_BASE];
+  const double ci = kr[KS_CI];
+  double p_shape = sp[FFB_S_P_BASE_SHAPE];
+  if (!isinf(ci)) {
+    const double penalty = (sp[FFB_S_KAPPA] * shape_log) / (1.0 + ci);
+    p_shape = sp[FFB_S_P_BASE_SHAPE] * (1.0 + penalty);
+  }
+  double p_pre = ((ca[CA_P_UNITS] + p_shape) + cb[CB_P_MEM]) + kr[KS_P_SM];
+  if (t_exec < sp[FFB_S_TAU_SHORT]) p_pre = p_pre * sp[FFB_S_TRANSIENT_R];         // power_model.py:93-95
+  *t_exec_out = t_exec; *p_pre_out = p_pre;
 }
 
 // ---- one cap of a unit (power_model.py:152-158, explorer.py:107); row = {scale, cap, max(0, cap - p_static), ok} ----

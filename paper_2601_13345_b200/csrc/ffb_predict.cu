@@ -16,6 +16,8 @@
 
 #include <string.h>
 #include <algorithm>
+#include <utility>
+#include <vector>
 
 using namespace ffbm;
 
@@ -184,6 +186,82 @@ predict_grid_kernel(GridArgs a) {
   }
 }
 
+// The streaming configuration (t / e only) with the factored model of ffb_model.cuh: one CTA per (kernel, spec)
+// group evaluates the group's class rows once - (threads, regs) classes and clipped-block_x classes - and then
+// walks the group's shapes 256 at a time: two fp64 divides per shape instead of ten (round 1: 780 thread
+// instructions per unit, 44% of the copy peak).  Same staging and coalesced write-out as predict_grid_kernel.
+constexpr int kGridMaxClassA = 512;
+__global__ void __launch_bounds__(kUnitsPerCta, 4)
+predict_grid_classes_kernel(GridArgs a) {
+  FFB_DYN_SMEM(smem_raw);
+  const int C = a.n_caps, J = a.n_shapes;
+  double* s_t = reinterpret_cast<double*>(smem_raw);            // [units][C]
+  double* s_e = s_t + (size_t)kUnitsPerCta * C;
+  double* s_ca = s_e + (size_t)kUnitsPerCta * C;                // [n_a][kClassAWidth]
+  double* s_cb = s_ca + (size_t)a.tb.n_a * kClassAWidth;        // [n_b][kClassBWidth]
+  const int64_t g = blockIdx.x;
+  const int64_t k = g / a.n_specs;
+  const int s = (int)(g - k * a.n_specs);
+  const double* f = a.feat + k * FFB_FEAT_WIDTH;
+  const double* sp = a.tb.spec + (size_t)s * FFB_SPEC_WIDTH;
+  const double* sd = a.tb.sd + (size_t)s * kSdWidth;
+  const double* kr = a.kstab + g * kKsWidth;
+  const int64_t shared_dyn = a.res[2 * k + 0], total_blocks = a.res[2 * k + 1];
+  const bool classes = f[FFB_F_OVR] == 0.0;
+  if (classes) {
+    for (int i = threadIdx.x; i < a.tb.n_a + a.tb.n_b; i += kUnitsPerCta) {
+      if (i < a.tb.n_a) eval_class_a(f, sp, sd, kr, a.tb.a_rep[2 * i], a.tb.a_rep[2 * i + 1], shared_dyn, total_blocks, s_ca + (size_t)i * kClassAWidth);
+      else eval_class_b(f, sp, sd, a.tb.b_rep[i - a.tb.n_a], s_cb + (size_t)(i - a.tb.n_a) * kClassBWidth);
+    }
+  }
+  __syncthreads();
+  const double p_static = sp[FFB_S_P_STATIC], e_over = sp[FFB_S_E_OVERHEAD];
+  const double2* ct2 = reinterpret_cast<const double2*>(a.tb.cap_tab + (size_t)s * C * 4);
+  for (int j0 = 0; j0 < J; j0 += kUnitsPerCta) {
+    const int j = j0 + threadIdx.x;
+    const int n_live = J - j0 < kUnitsPerCta ? J - j0 : kUnitsPerCta;
+    if (j < J) {
+      double t_exec, p_pre;
+      bool valid;
+      if (classes) {
+        const int32_t cls = a.tb.shape_cls[j];
+        const double* ca = s_ca + (size_t)(cls & 0xffff) * kClassAWidth;
+        eval_shape(sp, kr, ca, s_cb + (size_t)(cls >> 16) * kClassBWidth, a.tb.shape_log[j], &t_exec, &p_pre);
+        valid = ca[CA_VALID] != 0.0;
+      } else {
+        Unit u;
+        eval_unit(f, sp, sd, kr, a.tb.shape + 4 * j, a.tb.shape_log[j], shared_dyn, total_blocks, 0, u);
+        t_exec = u.t_exec; p_pre = u.p_pre; valid = u.valid;
+      }
+      for (int c = 0; c < C; ++c) {
+        const double2 sc_cap = ct2[2 * c], room_ok = ct2[2 * c + 1];
+        double p_dyn;
+        bool limited;
+        const double e_pred = eval_cap(t_exec, p_pre, p_static, e_over, sc_cap.x, sc_cap.y, room_ok.x, &p_dyn, &limited);
+        const bool ok = valid && room_ok.y != 0.0;
+        const size_t o = (size_t)threadIdx.x * C + c;
+        s_t[o] = ok ? t_exec : INFINITY;
+        s_e[o] = ok ? e_pred : INFINITY;
+      }
+    }
+    __syncthreads();
+    const int total = n_live * C;
+    const size_t base = ((size_t)g * J + j0) * C;
+    if ((base & 1) == 0) {
+      const int pairs = total >> 1;
+      double2* gt = reinterpret_cast<double2*>(a.t + base);
+      double2* ge = reinterpret_cast<double2*>(a.e + base);
+      const double2* st2 = reinterpret_cast<const double2*>(s_t);
+      const double2* se2 = reinterpret_cast<const double2*>(s_e);
+      for (int i = threadIdx.x; i < pairs; i += kUnitsPerCta) { gt[i] = st2[i]; ge[i] = se2[i]; }
+      if ((total & 1) && threadIdx.x == 0) { a.t[base + total - 1] = s_t[total - 1]; a.e[base + total - 1] = s_e[total - 1]; }
+    } else {
+      for (int i = threadIdx.x; i < total; i += kUnitsPerCta) { a.t[base + i] = s_t[i]; a.e[base + i] = s_e[i]; }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // ---- host side ----------------------------------------------------------------------------
@@ -226,7 +304,7 @@ int32_t ffb_build_tables(FfbContext* ctx, const double* h_spec_in, const int32_t
   const size_t n_spec = (size_t)S * FFB_SPEC_WIDTH, n_sd = (size_t)S * kSdWidth, n_log = (size_t)J,
                n_cap = (size_t)C, n_sc = (size_t)S * C, n_psm = (size_t)S * psm_n;
   const size_t n_dbl = n_spec + n_sd + n_log + n_cap + 7 * n_sc + n_psm;
-  const size_t bytes = n_dbl * sizeof(double) + (size_t)J * 4 * sizeof(int32_t);
+  const size_t bytes = n_dbl * sizeof(double) + (size_t)J * 8 * sizeof(int32_t);       // shapes [J,4] + class index [J] + class rows [<= 3J]
   // The tables are built in pageable memory first: a call whose tables equal the ones already on the
   // device (chunked pipelines score many kernel ranges against the same specs / shapes / caps) neither
   // uploads them again nor waits for the pinned staging buffer, so the host can keep enqueueing.
@@ -276,6 +354,32 @@ int32_t ffb_build_tables(FfbContext* ctx, const double* h_spec_in, const int32_t
       return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "shape %lld: block dims must be >= 1", (long long)j);
     h_log[j] = fabs(log((double)bx / (double)by));                             // power_model.py:61
   }
+  // shape classes of the factored model (ffb_model.cuh): unique (threads, regs) and unique min(block_x, 32)
+  int32_t* h_cls = h_shape + (size_t)J * 4;
+  int32_t* h_arep = h_cls + J;
+  int32_t* h_brep = h_arep + 2 * (size_t)J;
+  memset(h_cls, 0, (size_t)J * 4 * sizeof(int32_t));
+  int n_a = 0, n_b = 0;
+  {
+    std::vector<std::pair<std::pair<int64_t, int32_t>, int>> amap;             // small: linear search over the classes found so far
+    int bmap[33];
+    for (int i = 0; i < 33; ++i) bmap[i] = -1;
+    for (int64_t j = 0; j < J; ++j) {
+      const int64_t threads = (int64_t)h_shape[4 * j] * h_shape[4 * j + 1] * h_shape[4 * j + 2];
+      const int32_t regs = h_shape[4 * j + 3];
+      int ia = -1;
+      for (auto& kv : amap) if (kv.first.first == threads && kv.first.second == regs) { ia = kv.second; break; }
+      if (ia < 0) {
+        ia = n_a++;
+        amap.push_back({{threads, regs}, ia});
+        h_arep[2 * ia] = (int32_t)(threads > 0x7fffffff ? 0x7fffffff : threads); h_arep[2 * ia + 1] = regs;
+      }
+      const int bxc = h_shape[4 * j] < 32 ? h_shape[4 * j] : 32;
+      if (bmap[bxc] < 0) { bmap[bxc] = n_b; h_brep[n_b++] = bxc; }
+      h_cls[j] = ia | (bmap[bxc] << 16);
+      if (n_a > 4096) break;                                              // no use as classes: callers evaluate every shape
+    }
+  }
   if (!(ctx->tables_shadow_dev == ctx->d_tables.p && ctx->tables_shadow_stream == (void*)stream && ctx->tables_shadow.size() == bytes &&
         memcmp(ctx->tables_shadow.data(), scratch.data(), bytes) == 0)) {
     rc = ffb_stage_reserve(ctx, bytes);
@@ -301,6 +405,10 @@ int32_t ffb_build_tables(FfbContext* ctx, const double* h_spec_in, const int32_t
   tb.psm = tb.cap_ok + n_sc;
   tb.shape = (const int32_t*)(tb.psm + n_psm);
   tb.psm_n = psm_n;
+  tb.shape_cls = tb.shape + (size_t)J * 4;
+  tb.a_rep = tb.shape_cls + J;
+  tb.b_rep = tb.a_rep + 2 * (size_t)J;
+  tb.n_a = n_a <= 4096 ? n_a : 0; tb.n_b = n_b;           // n_a == 0: no class tables (callers fall back to eval_unit)
   *tb_out = tb;
   *host_err_out = host_err;
   return FFB_OK;
@@ -350,6 +458,11 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   if (g->d_detail) {
     FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FFB_LAUNCH((predict_grid_kernel<true, false>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
+  } else if (lean && a.t && a.e && a.cap_tile == (int)C && tb.n_a > 0 && tb.n_a <= kGridMaxClassA && K * S <= 0x7fffffffLL &&
+             smem + ((size_t)tb.n_a * kClassAWidth + (size_t)tb.n_b * kClassBWidth) * sizeof(double) <= 96 * 1024) {
+    const size_t smem_c = (size_t)kUnitsPerCta * C * 16 + ((size_t)tb.n_a * kClassAWidth + (size_t)tb.n_b * kClassBWidth) * sizeof(double);
+    FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_classes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+    FFB_LAUNCH(predict_grid_classes_kernel, (unsigned)(K * S), kUnitsPerCta, smem_c, stream, a);
   } else if (lean) {
     FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FFB_LAUNCH((predict_grid_kernel<false, true>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);

@@ -24,6 +24,30 @@ def _alt_spec():
     return a2, p2
 
 
+@pytest.mark.parametrize("axes", ["xy", "xyz_regs"])
+def test_streaming_grid_with_factored_model_equals_the_full_chain(backend, axes):
+    """t / e only (no flags, no status: the streaming configuration) takes the kernel that evaluates the group's
+    (threads, regs) and clipped-block_x class rows once and two divides per shape; every bit must equal the
+    per-shape chain of the general kernel, which the test above pins to the oracle.  Odd J x C sizes exercise
+    both write-out forms."""
+    K = 5 if backend == "emul" else 300
+    feat, res = synth.feature_rows(seed=17, n_kernels=K)
+    pairs = [(specs.default_architecture(), specs.default_calibration(), 65536 if axes == "xyz_regs" else 0), _alt_spec()]
+    sp = engine.spec_rows(pairs)
+    if axes == "xy":
+        shp = engine.shape_rows([tuple(x) for x in engine.enumerate_shapes(sp[0], 0, list(range(1, 1025)))][: (121 if backend == "emul" else 464)])
+    else:
+        pw = [1, 2, 4, 8, 16, 32, 64, 128]
+        shp = engine.shape_rows([(bx, by, bz, rg) for bx in pw for by in pw for bz in (1, 2, 3) for rg in (16, 64, 255)][: (275 if backend == "emul" else 10**6)])
+    caps = np.array([100.0, 125.0, 150.0, 200.0, 249.0, 250.0, 400.0])
+    d_feat, d_res = engine.features_tensor(feat), engine.resources_tensor(res)
+    full = engine.score_grid(d_feat, d_res, sp, shp, caps, want=("t", "e", "flags"))
+    lean = engine.score_grid(d_feat, d_res, sp, shp, caps, want=("t", "e"), check=False)
+    assert np.array_equal(_bits(full.t.cpu().numpy()), _bits(lean.t.cpu().numpy()))
+    assert np.array_equal(_bits(full.e.cpu().numpy()), _bits(lean.e.cpu().numpy()))
+    assert np.isfinite(lean.t.cpu().numpy()).any() and np.isinf(lean.t.cpu().numpy()).any()
+
+
 @pytest.mark.parametrize("case", ["default", "two_specs"])
 def test_grid_matches_oracle_bitwise(backend, case):
     K = 6 if backend == "emul" else 64
