@@ -511,27 +511,93 @@ Plan plan_groups(const FfbContext* ctx, int64_t group_size, bool has_tie, bool h
 // the buckets follows, pass 2 keeps a candidate unless a STRICTLY lower bucket holds a strictly smaller t -
 // i.e. unless it is provably dominated (explorer.py:122-140: drop iff some j has e_j < e_i and t_j < t_i).
 // NaNs neither dominate nor get dropped.  Survivors are compacted with their ids.
-constexpr int kPreBuckets = 4096;
+constexpr int kPreBuckets = 4096;                             // table entries: e-buckets x occupancy levels
 constexpr int kPreThreads = 512;
 constexpr int kPreRun = 4096;                                 // candidates per sampled run of pass 1
+constexpr int kPreLevels = 64;                                // distinct occupancy values the three-objective filter handles
+// Three objectives (drop i iff some j has e_j < e_i, t_j < t_i and occ_j >= occ_i): the table gets one column per
+// DISTINCT occupancy value (pass 0 collects them, at most kPreLevels; more: no pre-filter), min t per (e-bucket,
+// level); after the exclusive prefix-min over the buckets a suffix-min over the levels makes entry (b, l) the
+// smallest t among strictly lower e-buckets and occupancy >= level l.
 struct PreArgs {
-  const double* e; const double* t; const uint64_t* id;
+  const double* e; const double* t; const double* occ; const uint64_t* id;
   int64_t n;
   int64_t sample;                   // pass 1 reads every sample-th run of kPreRun candidates (1: all)
   double* range;                    // {lo, scale}
-  unsigned long long* gmin;         // [kPreBuckets] min t per bucket, later the exclusive prefix-min
-  double* out_e; double* out_t; uint64_t* out_id;
+  unsigned long long* gmin;         // [kPreBuckets] min t per (bucket, level), later the prefix / suffix minima
+  unsigned long long* lv_set;       // [2 * kPreLevels] hash set of ordered occupancy bits + 1 (pass 0)
+  double* lv;                       // [kPreLevels] the distinct occupancy values, ascending
+  int* n_lv;                        // their number (0: more than kPreLevels)
+  int levels, lshift;               // columns of the table (power of two >= *n_lv, fixed by the host after pass 0); log2
+  double* out_e; double* out_t; double* out_occ; uint64_t* out_id;
   int64_t out_cap;
   unsigned long long* out_count;
   uint32_t* overflow;
 };
-FFB_D int pre_bucket(double ev, double lo, double scale) {
+FFB_D int pre_bucket(double ev, double lo, double scale, int n_buckets) {
   const double x = (ev - lo) * scale;
   if (!(x > 0.0)) return 0;                                   // below the sampled range, or NaN
-  return x >= (double)(kPreBuckets - 1) ? kPreBuckets - 1 : (int)x;
+  return x >= (double)(n_buckets - 1) ? n_buckets - 1 : (int)x;
+}
+FFB_D int pre_level(double ov, const double* s_lv, int n_lv) {           // rank of ov among the distinct values (exact match exists)
+  int lo = 0, hi = n_lv - 1;
+  while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lv[mid] < ov) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+__global__ void __launch_bounds__(kPreThreads) pre_levels_kernel(PreArgs a) {
+  // pass 0 (three objectives): the distinct occupancy values, through a per-CTA set first
+  __shared__ unsigned long long s_set[2 * kPreLevels];
+  __shared__ int s_over;
+  for (int i = threadIdx.x; i < 2 * kPreLevels; i += kPreThreads) s_set[i] = 0ull;
+  if (threadIdx.x == 0) s_over = 0;
+  __syncthreads();
+  unsigned long long last = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kPreThreads) {
+    const double ov = a.occ[i] + 0.0;
+    const unsigned long long key = (unsigned long long)ordered_bits(ov) + 1ull;
+    if (key == last || ov != ov) continue;
+    last = key;
+    uint32_t s = (uint32_t)((key * 0x9e3779b97f4a7c15ull) >> 57);
+    for (int pr = 0; pr < 2 * kPreLevels; ++pr) {
+      const unsigned long long prev = atomicCAS(&s_set[s], 0ull, key);
+      if (prev == 0ull || prev == key) break;
+      s = (s + 1) & (2 * kPreLevels - 1);
+      if (pr == 2 * kPreLevels - 1) s_over = 1;
+    }
+  }
+  __syncthreads();
+  if (s_over) { *a.overflow = 1u; return; }
+  for (int i = threadIdx.x; i < 2 * kPreLevels; i += kPreThreads) {
+    const unsigned long long key = s_set[i];
+    if (!key) continue;
+    uint32_t s = (uint32_t)((key * 0x9e3779b97f4a7c15ull) >> 57);
+    for (int pr = 0; pr < 2 * kPreLevels; ++pr) {
+      const unsigned long long prev = atomicCAS(&a.lv_set[s], 0ull, key);
+      if (prev == 0ull || prev == key) break;
+      s = (s + 1) & (2 * kPreLevels - 1);
+      if (pr == 2 * kPreLevels - 1) *a.overflow = 1u;
+    }
+  }
+}
+__global__ void pre_levels_sort_kernel(PreArgs a) {            // one warp: <= 128 slots -> ascending distinct values
+  if (threadIdx.x != 0) return;
+  int n = 0;
+  double v[2 * kPreLevels];
+  for (int i = 0; i < 2 * kPreLevels; ++i) {
+    const unsigned long long key = a.lv_set[i];
+    if (!key) continue;
+    const unsigned long long ob = key - 1ull;
+    const unsigned long long bits = (ob & 0x8000000000000000ull) ? (ob & 0x7fffffffffffffffull) : ~ob;
+    v[n++] = __longlong_as_double((long long)bits);
+  }
+  if (n > kPreLevels || *a.overflow) { *a.n_lv = 0; return; }
+  for (int i = 1; i < n; ++i) { const double x = v[i]; int j = i - 1; while (j >= 0 && v[j] > x) { v[j + 1] = v[j]; --j; } v[j + 1] = x; }
+  for (int i = 0; i < n; ++i) a.lv[i] = v[i];
+  *a.n_lv = n;
 }
 __global__ void __launch_bounds__(1024) pre_range_kernel(PreArgs a) {
   __shared__ double s_lo[32], s_hi[32];
+  const int n_buckets = kPreBuckets >> a.lshift;
   const int64_t m = a.n < 65536 ? a.n : 65536;
   const int64_t stride = a.n / m;                             // sample spread over the whole set
   double lo = INFINITY, hi = -INFINITY;
@@ -549,13 +615,16 @@ __global__ void __launch_bounds__(1024) pre_range_kernel(PreArgs a) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = s_lo[w] < lo ? s_lo[w] : lo; hi = s_hi[w] > hi ? s_hi[w] : hi; }
     const double span = hi - lo;
     a.range[0] = lo < INFINITY ? lo : 0.0;
-    a.range[1] = (span > 0.0 && span < INFINITY) ? (double)kPreBuckets / span : 0.0;
+    a.range[1] = (span > 0.0 && span < INFINITY) ? (double)n_buckets / span : 0.0;
   }
   for (int b = threadIdx.x; b < kPreBuckets; b += blockDim.x) a.gmin[b] = ~0ull;
 }
 __global__ void __launch_bounds__(kPreThreads) pre_min_kernel(PreArgs a) {
   __shared__ unsigned long long s_min[kPreBuckets];
+  __shared__ double s_lv[kPreLevels];
+  const int n_buckets = kPreBuckets >> a.lshift, n_lv = a.occ ? *a.n_lv : 1;
   for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads) s_min[b] = ~0ull;
+  if (a.occ && threadIdx.x < n_lv) s_lv[threadIdx.x] = a.lv[threadIdx.x];
   __syncthreads();
   const double lo = a.range[0], scale = a.range[1];
   // every `sample`-th run of kPreRun candidates: a minimum over a SUBSET is still a valid certificate (the pass-2
@@ -565,41 +634,79 @@ __global__ void __launch_bounds__(kPreThreads) pre_min_kernel(PreArgs a) {
     const int64_t i = a.sample > 1 ? (j / kPreRun) * ((int64_t)kPreRun * a.sample) + (j % kPreRun) : j;
     const double ev = a.e[i], tv = a.t[i];
     if (ev != ev || tv != tv) continue;
-    const int b = pre_bucket(ev, lo, scale);
+    int slot = pre_bucket(ev, lo, scale, n_buckets);
+    if (a.occ) {
+      const double ov = a.occ[i] + 0.0;
+      if (ov != ov) continue;
+      slot = (slot << a.lshift) | pre_level(ov, s_lv, n_lv);
+    }
     const unsigned long long tb = (unsigned long long)ordered_bits(tv);
-    if (tb < s_min[b]) atomicMin(&s_min[b], tb);            // the plain read only spares atomics that cannot win
+    if (tb < s_min[slot]) atomicMin(&s_min[slot], tb);        // the plain read only spares atomics that cannot win
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads)
     if (s_min[b] != ~0ull) atomicMin(&a.gmin[b], s_min[b]);
 }
 __global__ void __launch_bounds__(1024) pre_prefix_kernel(PreArgs a) {
-  // exclusive prefix-min over kPreBuckets values: 4 per thread, warp scan, scan of the warp totals
+  __shared__ unsigned long long s_tab[kPreBuckets];
   __shared__ unsigned long long s_w[32];
   const int tid = threadIdx.x;
-  unsigned long long v[4], run = ~0ull;
-  for (int k = 0; k < 4; ++k) { v[k] = a.gmin[4 * tid + k]; }
-  unsigned long long tot = v[0] < v[1] ? v[0] : v[1];
-  tot = v[2] < tot ? v[2] : tot; tot = v[3] < tot ? v[3] : tot;
-  unsigned long long incl = tot;
-  for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, d); if ((tid & 31) >= d && o < incl) incl = o; }
-  if ((tid & 31) == 31) s_w[tid >> 5] = incl;
+  if (a.lshift == 0) {
+    // two objectives: exclusive prefix-min over kPreBuckets values, 4 per thread, warp scan, scan of the warp totals
+    unsigned long long v[4], run = ~0ull;
+    for (int k = 0; k < 4; ++k) { v[k] = a.gmin[4 * tid + k]; }
+    unsigned long long tot = v[0] < v[1] ? v[0] : v[1];
+    tot = v[2] < tot ? v[2] : tot; tot = v[3] < tot ? v[3] : tot;
+    unsigned long long incl = tot;
+    for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, d); if ((tid & 31) >= d && o < incl) incl = o; }
+    if ((tid & 31) == 31) s_w[tid >> 5] = incl;
+    __syncthreads();
+    if (tid < 32) {
+      unsigned long long w = s_w[tid], wi = w;
+      for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, d); if (tid >= d && o < wi) wi = o; }
+      const unsigned long long ex = __shfl_up_sync(0xffffffffu, wi, 1);
+      s_w[tid] = tid == 0 ? ~0ull : ex;
+    }
+    __syncthreads();
+    unsigned long long before = __shfl_up_sync(0xffffffffu, incl, 1);
+    if ((tid & 31) == 0) before = ~0ull;
+    run = before < s_w[tid >> 5] ? before : s_w[tid >> 5];
+    for (int k = 0; k < 4; ++k) { a.gmin[4 * tid + k] = run; run = v[k] < run ? v[k] : run; }
+    return;
+  }
+  // three objectives, in shared memory: per level an exclusive prefix-min over the e-buckets (thread l walks column
+  // l), then per bucket a suffix-min over the levels (occupancy >= level)
+  const int levels = 1 << a.lshift, n_buckets = kPreBuckets >> a.lshift;
+  for (int i = tid; i < kPreBuckets; i += blockDim.x) s_tab[i] = a.gmin[i];
   __syncthreads();
-  if (tid < 32) {
-    unsigned long long w = s_w[tid], wi = w;
-    for (int d = 1; d < 32; d <<= 1) { const unsigned long long o = __shfl_up_sync(0xffffffffu, wi, d); if (tid >= d && o < wi) wi = o; }
-    const unsigned long long ex = __shfl_up_sync(0xffffffffu, wi, 1);
-    s_w[tid] = tid == 0 ? ~0ull : ex;
+  if (tid < levels) {
+    unsigned long long run = ~0ull;
+    for (int b = 0; b < n_buckets; ++b) {
+      const int at = (b << a.lshift) | tid;
+      const unsigned long long v = s_tab[at];
+      s_tab[at] = run;
+      run = v < run ? v : run;
+    }
   }
   __syncthreads();
-  unsigned long long before = __shfl_up_sync(0xffffffffu, incl, 1);
-  if ((tid & 31) == 0) before = ~0ull;
-  run = before < s_w[tid >> 5] ? before : s_w[tid >> 5];
-  for (int k = 0; k < 4; ++k) { a.gmin[4 * tid + k] = run; run = v[k] < run ? v[k] : run; }
+  for (int b = tid; b < n_buckets; b += blockDim.x) {
+    unsigned long long run = ~0ull;
+    for (int l = levels - 1; l >= 0; --l) {
+      const int at = (b << a.lshift) | l;
+      const unsigned long long v = s_tab[at];
+      run = v < run ? v : run;
+      s_tab[at] = run;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < kPreBuckets; i += blockDim.x) a.gmin[i] = s_tab[i];
 }
 __global__ void __launch_bounds__(kPreThreads) pre_filter_kernel(PreArgs a) {
   __shared__ unsigned long long s_pm[kPreBuckets];
+  __shared__ double s_lv[kPreLevels];
+  const int n_buckets = kPreBuckets >> a.lshift, n_lv = a.occ ? *a.n_lv : 1;
   for (int b = threadIdx.x; b < kPreBuckets; b += kPreThreads) s_pm[b] = a.gmin[b];
+  if (a.occ && threadIdx.x < n_lv) s_lv[threadIdx.x] = a.lv[threadIdx.x];
   __syncthreads();
   const double lo = a.range[0], scale = a.range[1];
   const int lane = threadIdx.x & 31;
@@ -607,10 +714,16 @@ __global__ void __launch_bounds__(kPreThreads) pre_filter_kernel(PreArgs a) {
   const int64_t n_round = (a.n + step - 1) / step * step;     // whole warps take part in every ballot
   for (int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x; i < n_round; i += step) {
     bool keep = false;
-    double ev = 0.0, tv = 0.0;
+    double ev = 0.0, tv = 0.0, ov = 0.0;
     if (i < a.n) {
       ev = a.e[i]; tv = a.t[i];
-      keep = ev != ev || tv != tv || !(s_pm[pre_bucket(ev, lo, scale)] < (unsigned long long)ordered_bits(tv));
+      if (a.occ) ov = a.occ[i];
+      keep = ev != ev || tv != tv || ov != ov;
+      if (!keep) {
+        int slot = pre_bucket(ev, lo, scale, n_buckets);
+        if (a.occ) slot = (slot << a.lshift) | pre_level(ov + 0.0, s_lv, n_lv);
+        keep = !(s_pm[slot] < (unsigned long long)ordered_bits(tv));
+      }
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (!m) continue;
@@ -619,7 +732,10 @@ __global__ void __launch_bounds__(kPreThreads) pre_filter_kernel(PreArgs a) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (keep) {
       const int64_t at = (int64_t)base + __popc(m & ((1u << lane) - 1u));
-      if (at < a.out_cap) { a.out_e[at] = ev; a.out_t[at] = tv; a.out_id[at] = a.id ? a.id[i] : (uint64_t)i; }
+      if (at < a.out_cap) {
+        a.out_e[at] = ev; a.out_t[at] = tv; a.out_id[at] = a.id ? a.id[i] : (uint64_t)i;
+        if (a.occ) a.out_occ[at] = ov;
+      }
       else *a.overflow = 1u;
     }
   }
@@ -702,7 +818,7 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   if (work_cap < cap_front) work_cap = cap_front;
   // scratch: two ping-pong triples + counters/status
   const size_t tri = (size_t)work_cap * (d_occ ? 32 : 24);
-  int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 2 * tri + 256 + (size_t)kPreBuckets * 8 + 64);
+  int32_t rc = ffb_reserve(ctx, &ctx->d_sky, 2 * tri + 256 + (size_t)kPreBuckets * 8 + 64 + (size_t)3 * kPreLevels * 8 + 64);
   if (rc) return rc;
   char* base = (char*)ctx->d_sky.p;
   double* buf_e[2] = {(double*)base, (double*)(base + tri)};
@@ -721,29 +837,50 @@ extern "C" int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double*
   FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
   int64_t pre_min = (int64_t)1 << 20;
   if (const char* ev = getenv("FFB_SKYLINE_PREFILTER_MIN")) pre_min = atoll(ev);      // test hook: small sets through the pre-filter
-  if (!d_occ && n >= pre_min) {
-    // large two-objective sets: the streaming pre-filter first (see above); when its survivors do not fit the work
-    // buffer (a set that is mostly front) the levels below start from the whole set as before
+  if (n >= pre_min) {
+    // large sets: the streaming pre-filter first (see above); when its survivors do not fit the work buffer (a set
+    // that is mostly front), or a three-objective set has more than kPreLevels distinct occupancy values, the levels
+    // below start from the whole set as before
     PreArgs pa = {};
-    pa.e = d_e; pa.t = d_t; pa.id = d_id; pa.n = n;
+    pa.e = d_e; pa.t = d_t; pa.occ = d_occ; pa.id = d_id; pa.n = n;
     pa.sample = n >= ((int64_t)1 << 26) ? 16 : 1;
-    pa.gmin = (unsigned long long*)(base + 2 * tri + 256); pa.range = (double*)(base + 2 * tri + 256 + (size_t)kPreBuckets * 8);
-    pa.out_e = buf_e[0]; pa.out_t = buf_t[0]; pa.out_id = buf_id[0]; pa.out_cap = work_cap;
+    char* pbase = base + 2 * tri + 256;
+    pa.gmin = (unsigned long long*)pbase; pa.range = (double*)(pbase + (size_t)kPreBuckets * 8);
+    pa.lv_set = (unsigned long long*)(pbase + (size_t)kPreBuckets * 8 + 64);
+    pa.lv = (double*)(pa.lv_set + 2 * kPreLevels);
+    pa.n_lv = (int*)(pa.lv + kPreLevels);
+    pa.out_e = buf_e[0]; pa.out_t = buf_t[0]; pa.out_id = buf_id[0]; pa.out_occ = d_occ ? buf_occ[0] : nullptr; pa.out_cap = work_cap;
     pa.out_count = d_count + 3; pa.overflow = d_status + 1;
     unsigned ctas = (unsigned)ctx->sm_count * 4;
     if ((int64_t)ctas * kPreThreads > n) ctas = (unsigned)((n + kPreThreads - 1) / kPreThreads);
-    FFB_LAUNCH(pre_range_kernel, 1, 1024, 0, stream, pa);
-    FFB_LAUNCH(pre_min_kernel, ctas, kPreThreads, 0, stream, pa);
-    FFB_LAUNCH(pre_prefix_kernel, 1, 1024, 0, stream, pa);
-    FFB_LAUNCH(pre_filter_kernel, ctas, kPreThreads, 0, stream, pa);
-    rc = ffb_check_launch(ctx, "skyline pre-filter");
-    if (rc) return rc;
-    unsigned long long h_kept = 0; uint32_t h_over = 0;
-    FFB_CUDA(ctx, cudaMemcpyAsync(&h_kept, pa.out_count, sizeof(h_kept), cudaMemcpyDeviceToHost, stream));
-    FFB_CUDA(ctx, cudaMemcpyAsync(&h_over, pa.overflow, sizeof(h_over), cudaMemcpyDeviceToHost, stream));
-    FFB_CUDA(ctx, cudaStreamSynchronize(stream));
-    if (!h_over && (int64_t)h_kept <= work_cap) {
-      cur_e = buf_e[0]; cur_t = buf_t[0]; cur_id = buf_id[0]; cur_n = (int64_t)h_kept; which = 1;
+    bool usable = true;
+    if (d_occ) {
+      FFB_CUDA(ctx, cudaMemsetAsync(pa.lv_set, 0, (size_t)2 * kPreLevels * 8 + (size_t)kPreLevels * 8 + 16, stream));
+      FFB_LAUNCH(pre_levels_kernel, ctas, kPreThreads, 0, stream, pa);
+      FFB_LAUNCH(pre_levels_sort_kernel, 1, 32, 0, stream, pa);
+      int h_lv = 0;
+      FFB_CUDA(ctx, cudaMemcpyAsync(&h_lv, pa.n_lv, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      FFB_CUDA(ctx, cudaStreamSynchronize(stream));
+      usable = h_lv > 0;
+      while ((1 << pa.lshift) < h_lv) ++pa.lshift;
+      pa.levels = 1 << pa.lshift;
+      FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));       // the overflow flag of pass 0 shares the status word
+    }
+    if (usable) {
+      FFB_LAUNCH(pre_range_kernel, 1, 1024, 0, stream, pa);
+      FFB_LAUNCH(pre_min_kernel, ctas, kPreThreads, 0, stream, pa);
+      FFB_LAUNCH(pre_prefix_kernel, 1, 1024, 0, stream, pa);
+      FFB_LAUNCH(pre_filter_kernel, ctas, kPreThreads, 0, stream, pa);
+      rc = ffb_check_launch(ctx, "skyline pre-filter");
+      if (rc) return rc;
+      unsigned long long h_kept = 0; uint32_t h_over = 0;
+      FFB_CUDA(ctx, cudaMemcpyAsync(&h_kept, pa.out_count, sizeof(h_kept), cudaMemcpyDeviceToHost, stream));
+      FFB_CUDA(ctx, cudaMemcpyAsync(&h_over, pa.overflow, sizeof(h_over), cudaMemcpyDeviceToHost, stream));
+      FFB_CUDA(ctx, cudaStreamSynchronize(stream));
+      if (!h_over && (int64_t)h_kept <= work_cap) {
+        cur_e = buf_e[0]; cur_t = buf_t[0]; cur_id = buf_id[0]; cur_n = (int64_t)h_kept; which = 1;
+        if (d_occ) cur_occ = buf_occ[0];
+      }
     }
     FFB_CUDA(ctx, cudaMemsetAsync(d_count, 0, 128, stream));
   }

@@ -152,7 +152,10 @@ def test_three_objective_groups_match_oracle(backend, levels, rho):
             assert want == orc.pareto_indices(e[sl], t[sl], tie=tie, rho=rho)[0]
 
 
-def test_three_objective_large_set_and_capacity(backend):
+@pytest.mark.parametrize("prefilter", [False, True])
+def test_three_objective_large_set_and_capacity(backend, prefilter, monkeypatch):
+    # with the pre-filter: one table column per distinct occupancy value (8 here), also with the rho floor below
+    monkeypatch.setenv("FFB_SKYLINE_PREFILTER_MIN", "1000" if prefilter else str(1 << 40))
     n = 20_000 if backend == "emul" else 2_000_000
     rng = np.random.default_rng(77)
     e, t = rng.uniform(0.0, 10.0, n), rng.uniform(0.0, 10.0, n)
