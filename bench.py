@@ -120,6 +120,12 @@ def main():
     import torch.distributed as dist
     from paper_2601_13345_b200 import engine, native, specs, synth
 
+    # the corpus text is generated by a process pool BEFORE the CUDA context and the process group exist
+    corpus_parts = None
+    if not args.tiled_corpus and (args.corpus_mb != 0):
+        from paper_2601_13345_b200 import corpus as _cm
+        corpus_parts = _cm.generate_unique(4 + rank, args.kernels, irregular=args.irregular, workers=max(1, (os.cpu_count() or 1) // max(world, 1)))
+
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -155,7 +161,8 @@ def main():
         if args.tiled_corpus:
             corpus = corpus_mod.bench_corpus(seed=4 + rank, target_bytes=corpus_mb * 10**6, n_kernels=K)
         else:
-            corpus = corpus_mod.bench_corpus_unique(seed=4 + rank, n_kernels=K, irregular=args.irregular)
+            corpus = corpus_mod.bench_corpus_unique(seed=4 + rank, n_kernels=K, irregular=args.irregular, parts=corpus_parts)
+            corpus_parts = None
 
     h_feat = torch.from_numpy(feat_np).pin_memory()
     h_res = torch.from_numpy(res_np).pin_memory()

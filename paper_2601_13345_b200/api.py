@@ -518,15 +518,23 @@ def evaluate_configs(module: PtxModule, cfg: ControlFlowGraph, arch: Architectur
                           engine.resources_tensor([[resources.shared_mem_bytes, resources.total_blocks]]),
                           engine.spec_rows([(arch, profile)]), engine.shape_rows(shapes), np.asarray(caps),
                           want=("detail",), strict=True)
-    det = r.detail.cpu().numpy()[0, 0]
-    out = []
+    det = r.detail.cpu().numpy()[0, 0].tolist()          # [shape][cap][DETAIL_WIDTH] as Python floats: one conversion, not 21 per row
+    D = _N
+    isfinite = math.isfinite
+    out, keys = [], []
     for c in configs:
-        d = det[s_idx[(c.block_x, c.block_y)], c_idx[float(c.p_cap)]]
-        if not (math.isfinite(d[_N.D_T_EXEC]) and math.isfinite(d[_N.D_E_PRED])):
+        d = det[s_idx[(c.block_x, c.block_y)]][c_idx[float(c.p_cap)]]
+        t_exec, e_pred = d[D.D_T_EXEC], d[D.D_E_PRED]
+        if not (isfinite(t_exec) and isfinite(e_pred)):
             # IEEE gives inf / nan where CPython raises (a zero divisor such as ipc = 0, time_model.py:116)
             raise ZeroDivisionError("float division by zero")
-        out.append(Prediction(config=c, time=_time_of(d), power=_power_of(d), e_pred=float(d[_N.D_E_PRED])))
-    out.sort(key=lambda p: _config_key(p.config))
+        out.append(Prediction(c, TimeBreakdown(d[D.D_MWP], d[D.D_CWP], d[D.D_BW_EFF], d[D.D_T_MEM], d[D.D_T_COMP], d[D.D_T_SYNC], t_exec),
+                              PowerBreakdown(d[D.D_P_UNITS], d[D.D_P_SHAPE], d[D.D_P_MEM], d[D.D_P_SM], d[D.D_P_DYN], d[D.D_F_ADJ], d[D.D_CI],
+                                             int(d[D.D_ACTIVE_SMS]), d[D.D_CAP_LIMITED] != 0.0), e_pred))
+        keys.append((c.block_x * c.block_y, c.block_x, c.block_y, c.p_cap))
+    if any(keys[i] > keys[i + 1] for i in range(len(keys) - 1)):     # explorer.py:182; generate_valid_configs' order needs no sort
+        order = sorted(range(len(out)), key=keys.__getitem__)
+        out = [out[i] for i in order]
     return out
 
 
@@ -534,8 +542,10 @@ def _front_order(predictions: list[Prediction], rho: float):
     n = len(predictions)
     e = np.fromiter((p.e_pred for p in predictions), dtype=np.float64, count=n)
     t = np.fromiter((p.time.t_exec for p in predictions), dtype=np.float64, count=n)
-    keys = sorted(range(n), key=lambda i: (predictions[i].config.block_x, predictions[i].config.block_y,
-                                           predictions[i].config.p_cap, i))
+    cfgs = [p.config for p in predictions]
+    keys = np.lexsort((np.arange(n), np.fromiter((c.p_cap for c in cfgs), dtype=np.float64, count=n),
+                       np.fromiter((c.block_y for c in cfgs), dtype=np.int64, count=n),
+                       np.fromiter((c.block_x for c in cfgs), dtype=np.int64, count=n)))     # (block_x, block_y, p_cap, position)
     tie = np.empty(n, dtype=np.int32)
     tie[keys] = np.arange(n, dtype=np.int32)
     rt = native.get_runtime()

@@ -354,18 +354,26 @@ def _gen_piece(args):
     return synth.ptx_corpus(seed, count, irregular=irregular, first=first)
 
 
-def bench_corpus_unique(seed: int, n_kernels: int, *, irregular: float = 0.0, workers: int | None = None, piece: int = 600,
-                        rt: native.Runtime | None = None) -> Corpus:
-    """``n_kernels`` DIFFERENT generated kernels (no tiling): the text is produced in pieces of ``piece`` kernels by a
-    process pool (every piece has its own seed, names are unique over the corpus) and uploaded piece by piece.
-    ``irregular``: share of kernels with one construct that only the exact walk parses (synth.ptx_corpus)."""
+def generate_unique(seed: int, n_kernels: int, *, irregular: float = 0.0, workers: int | None = None, piece: int = 600):
+    """Host side of ``bench_corpus_unique``: [(text, offsets)] pieces of ``piece`` kernels each, produced by a process
+    pool (every piece has its own seed, names are unique over the corpus).  Touches no CUDA state, so it can run
+    before the device context and the process group exist."""
     import multiprocessing as mp
     import os
-    rt = rt or native.get_runtime()
     jobs = [(seed * 100_003 + i, i * piece, min(piece, n_kernels - i * piece), irregular) for i in range((n_kernels + piece - 1) // piece)]
-    workers = workers or min(len(jobs), os.cpu_count() or 1)
+    workers = max(1, min(len(jobs), workers or os.cpu_count() or 1))
     with mp.get_context("fork").Pool(workers) as pool:
-        parts = pool.map(_gen_piece, jobs)
+        return pool.map(_gen_piece, jobs)
+
+
+def bench_corpus_unique(seed: int, n_kernels: int, *, irregular: float = 0.0, workers: int | None = None, piece: int = 600,
+                        rt: native.Runtime | None = None, parts=None) -> Corpus:
+    """``n_kernels`` DIFFERENT generated kernels (no tiling), uploaded piece by piece (``parts``: the output of
+    ``generate_unique`` when the text was produced earlier).
+    ``irregular``: share of kernels with one construct that only the exact walk parses (synth.ptx_corpus)."""
+    if parts is None:
+        parts = generate_unique(seed, n_kernels, irregular=irregular, workers=workers, piece=piece)
+    rt = rt or native.get_runtime()
     total = sum(len(p[0]) for p in parts)
     padded = (total + 15) // 16 * 16 + 16
     dev = torch.full((padded,), 10, dtype=torch.uint8, device=rt.device)
