@@ -33,7 +33,7 @@ namespace {
 constexpr int kFlowWarps = 4;
 constexpr int kMapSlots = 512;                    // shared-memory register -> scale map per warp (8 KB)
 constexpr int kMapFill = 384;
-constexpr int kBodyList = 96;                     // loop bodies up to this many blocks are scanned through a compact list                     // entries kept on chip; later names spill to the HBM table
+constexpr int kBodyList = 32;                     // loop bodies up to this many blocks are scanned through a compact list                     // entries kept on chip; later names spill to the HBM table
 constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
 constexpr uint32_t kNoBlock = 0xffffffffu;
@@ -333,7 +333,7 @@ FFB_D double warp_sum_d(double v) {
 // "last match" scans of the trip recogniser, weights, record staging.  Lane 0 alone: the graph
 // walks (DFS, dominators, loop bodies) and the textual dataflow pass, which are sequential by
 // nature.
-__global__ void __launch_bounds__(kFlowWarps * 32, 5)
+__global__ void __launch_bounds__(kFlowWarps * 32, 6)
 flow_kernel(FlowArgs a) {
   __shared__ uint64_t s_ckey[kFlowWarps][kMapSlots];
   __shared__ int64_t s_cval[kFlowWarps][kMapSlots];
@@ -812,11 +812,19 @@ flow_kernel(FlowArgs a) {
           else S = st.get(h);                                                                     \
         }                                                                                         \
       }
-      FFB_RESOLVE(op1, sc.s1, p1)
-      FFB_RESOLVE(op2, sc.s2, p2)
-      FFB_RESOLVE(op3, sc.s3, p3)
-      FFB_RESOLVE(aux, sc.sa, pa)
+      // a memory statement reads one scale only - the address register of a global access (alignment.py:137-144);
+      // what it defines does not depend on its operands (:84-88).  Everything else may read all four.
+      const bool wants_addr = is_mem && ffb_meta_space(m) == FFB_SP_GLOBAL && ffb_meta_addr(m) == FFB_ADDR_REG;
+      sc.s1 = sc.s2 = sc.s3 = sc.sa = kNoneScale;
+      if (!is_mem && defines) {
+        FFB_RESOLVE(op1, sc.s1, p1)
+        FFB_RESOLVE(op2, sc.s2, p2)
+        FFB_RESOLVE(op3, sc.s3, p3)
+      }
+      if (wants_addr || (!is_mem && defines)) FFB_RESOLVE(aux, sc.sa, pa)
 #undef FFB_RESOLVE
+      // statements whose contribution needs no scale are counted here, once, with all lanes together
+      if (live && !wants_addr) count_statement(m, wgt, kNoneScale, acc);
       // waves: a statement runs once the lanes it depends on have published
       bool mine_done = !live;
       int64_t v = kNoneScale;
@@ -830,7 +838,7 @@ flow_kernel(FlowArgs a) {
           if (is_mem) v = ffb_meta_space(m) == FFB_SP_PARAM ? 0 : kNoneScale;            // alignment.py:84-88
           else if (defines) defines = eval_def(m, op1, op2, op3, sc, &v, &status);
           if (defines) ch_val[lane] = v;
-          count_statement(m, wgt, sc.sa, acc);
+          if (wants_addr) count_statement(m, wgt, sc.sa, acc);
           mine_done = true;
         }
         __syncwarp();
