@@ -17,7 +17,7 @@ for k in lex_fast flow_kernel explore_groups; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_${k}_$TAG python bench.py --steps 1 --warmup 1 --no-cpu-baseline --nvcc-mb 0 --irregular-leg 0 > gpurun_out/b_ncu_${k}_$TAG.log 2>&1; tail -1 gpurun_out/b_ncu_${k}_$TAG.log
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:lex_fast -s 2 -c 1 -o gpurun_out/prof_lex_fast_hist_$TAG python scripts/prof_hist.py > gpurun_out/b_ncu_hist_$TAG.log 2>&1; tail -1 gpurun_out/b_ncu_hist_$TAG.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:predict_grid -s 2 -c 1 -o gpurun_out/prof_predict_grid_$TAG python bench.py --workload grid_c3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/b_ncu_grid_$TAG.log 2>&1; tail -1 gpurun_out/b_ncu_grid_$TAG.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:predict_grid -s 4 -c 1 -o gpurun_out/prof_predict_grid_$TAG python bench.py --workload grid_c3 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/b_ncu_grid_$TAG.log 2>&1; tail -1 gpurun_out/b_ncu_grid_$TAG.log
 for k in pre_min pre_filter; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_${k}_$TAG python bench.py --workload front1e9 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/b_ncu_${k}_$TAG.log 2>&1; tail -1 gpurun_out/b_ncu_${k}_$TAG.log
 done
