@@ -232,8 +232,12 @@ def main():
                 h_front_n[s0:s1].copy_(fn[s0:s1], non_blocking=True)
                 h_front_off[s0:s1].copy_(fo[s0:s1], non_blocking=True)
 
-        lex_state.run(resident=False, on_chunk=on_chunk)
+        lex_state.run(resident=False, on_chunk=on_chunk, timeline=e2e.get("timeline"))
         main.wait_stream(side)                                    # the step ends when the last fronts are on the host
+        if e2e.get("timeline") is not None:
+            evt = torch.cuda.Event(enable_timing=True)
+            evt.record(main)
+            e2e["timeline"].append(("fronts on host", evt))
         return None, (e2e["front"], fn)
 
     def step(resident: bool, timed: bool):
@@ -311,6 +315,16 @@ def main():
     clocks = sampler.stop() if rank == 0 else None
     ms_e2e, _, _ = run(False, max(3, args.steps // 2), 2)
     e2e_steps = max(3, args.steps // 2)
+    # one more streamed step with timing events on both streams: where the step's time goes (ms since its start)
+    e2e_timeline = None
+    if corpus is not None and e2e.get("regions"):
+        torch.cuda.synchronize()
+        e2e["timeline"] = []
+        step(False, False)
+        torch.cuda.synchronize()
+        t0 = e2e["timeline"][0][1]
+        e2e_timeline = {label: round(t0.elapsed_time(evn), 2) for label, evn in e2e["timeline"][1:]}
+        e2e["timeline"] = None
     # the floor of the e2e leg: the same pinned host -> device copy of the corpus with nothing else running
     h2d_alone_ms = None
     if corpus is not None and lex_state.host_text is not None:
@@ -533,7 +547,8 @@ def main():
                                           + h_front_n.numel() * 4 + h_front_off.numel() * 8) * world,
                 "pipeline": (f"{len(e2e['regions'])} chunks of <= {args.e2e_chunk_mb} MB: upload, K1+K1b, K2+K3, K4 and the front read-back overlap"
                              if e2e.get("regions") else "none"),
-                "ms_per_step": ms_e2e / e2e_steps, "steps": e2e_steps, "h2d_alone_ms": h2d_alone_ms},
+                "ms_per_step": ms_e2e / e2e_steps, "steps": e2e_steps, "h2d_alone_ms": h2d_alone_ms,
+                "timeline_ms": e2e_timeline},
         "roofline": roofline, "cpu_baseline": cpu,
     }
     print(json.dumps(out))

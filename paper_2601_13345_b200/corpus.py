@@ -434,27 +434,41 @@ class StreamedAnalysis:
         self.copy_stream = torch.cuda.Stream(device=rt.device) if rt.device.type == "cuda" else None
         self.events = [torch.cuda.Event() for _ in bounds] if self.copy_stream is not None else []
 
-    def run(self, default_trip: float = 32.0, on_chunk=None) -> torch.Tensor:
+    def run(self, default_trip: float = 32.0, on_chunk=None, timeline: list | None = None) -> torch.Tensor:
         """``on_chunk(c, s0, s1)`` runs on the compute stream right after chunk c's feature rows are
-        enqueued (e.g. to score and rank those kernels while later chunks are still uploading)."""
+        enqueued (e.g. to score and rank those kernels while later chunks are still uploading).
+        ``timeline``: when a list, timing events are appended as (label, event) - one after every chunk's
+        upload (copy stream) and after its lexer / dataflow / on_chunk work (compute stream)."""
         rt, corp = self.rt, self.corp
+
+        def mark(label, stream=None):
+            if timeline is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream if stream is not None else torch.cuda.current_stream(rt.device))
+                timeline.append((label, ev))
+
         if self.copy_stream is not None:
             main = torch.cuda.current_stream(rt.device)
+            mark("start")
             self.copy_stream.wait_stream(main)            # earlier readers of the text buffer are done
             with torch.cuda.stream(self.copy_stream):
-                for (lo, hi), ev in zip(self.ranges, self.events):
+                for c, ((lo, hi), ev) in enumerate(zip(self.ranges, self.events)):
                     corp.text[lo:hi].copy_(self.host[lo:hi], non_blocking=True)
                     ev.record(self.copy_stream)
+                    mark(f"h2d[{c}]", self.copy_stream)
         else:
             corp.text.copy_(self.host)
         for c, (s0, s1) in enumerate(self.bounds):
             if self.copy_stream is not None:
                 torch.cuda.current_stream(rt.device).wait_event(self.events[c])
             lex_records_single_pass(corp, out=self.lex, rt=rt, seg_range=(s0, s1), order=self.orders[c])
+            mark(f"lex[{c}]")
             kernel_features(corp, self.lex, default_trip=default_trip, out_feat=self.feat, out_status=self.status, rt=rt,
                             seg_range=(s0, s1), order=self.orders[c])
+            mark(f"flow[{c}]")
             if on_chunk is not None:
                 on_chunk(c, s0, s1)
+                mark(f"score+front[{c}]")
         return self.feat
 
 
@@ -476,14 +490,14 @@ class BenchLexState:
             self.host_text.copy_(self.corp.text)
         return self.host_text
 
-    def run(self, resident: bool = True, mark=None, on_chunk=None) -> torch.Tensor:
+    def run(self, resident: bool = True, mark=None, on_chunk=None, timeline: list | None = None) -> torch.Tensor:
         rt, corp = self.rt, self.corp
         if not resident:
             # host text -> feature rows through the public streamed path: H2D inside the timed
             # region, overlapped chunk by chunk with K1 / K1b
             if self.streamed is None:
                 self.streamed = StreamedAnalysis(rt, corp, self.pin_host(), lex=self.lex, feat=self.feat, chunk_bytes=self.chunk_bytes)
-            self.streamed.run(on_chunk=on_chunk)
+            self.streamed.run(on_chunk=on_chunk, timeline=timeline)
             if mark is not None:
                 mark.record()
             return self.feat
