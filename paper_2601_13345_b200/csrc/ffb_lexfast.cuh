@@ -310,18 +310,30 @@ FFB_D bool address_fast(const uint8_t* s, int a, int b, uint32_t* kind, uint64_t
 
 // ---- opcode memo ----------------------------------------------------------------------------------
 // PTX repeats a few hundred opcode strings ("ld.global.f32", "mad.lo.s32" ...).  classify_opcode
-// (ptx.py:99-136) depends on that string alone, so every CTA keeps a small table  text (<= 24 bytes,
-// compared exactly) -> opcode part of the meta word  in shared memory: a statement costs one probe
-// instead of a token loop.  Entries are written once and never change: a writer claims the slot's
-// state word, stores the first half of the key, then (after a fence) the half that carries the
-// value with its valid bit; a reader loads that half first.
-constexpr int kMemoSlots = 256;
+// (ptx.py:99-136) depends on that string alone, so every CTA keeps a table  text (compared exactly) ->
+// opcode part of the meta word  in shared memory: a statement costs one probe instead of a token loop.
+// Two tables: 256 slots of 32 B for opcodes of at most 24 bytes, 32 slots of 64 B for 25..56 bytes (mma / tex /
+// wmma shapes); longer opcodes always take the token walk.
+// The table is READ while tiles are parsed and WRITTEN only between two CTA barriers: a lane that misses
+// classifies its opcode with the token walk and queues (key, value); behind the barrier that paces the tile loop
+// every thread sees the queue length of the finished iteration (two queues, alternating, so nobody can be writing
+// the one being read), one lane enters the queued opcodes, a second barrier ends the insert phase.  No atomics on
+// the table, no fences, nothing for racecheck to flag - and 512 lanes missing `add.s32` at once leave one entry.
+constexpr int kMemoSlots = 256, kMemoProbes = 8;
+constexpr int kLongSlots = 32, kLongProbes = 4, kLongWords = 14;
+constexpr int kPendMax = 32;                                    // queued inserts per iteration (more: retried later)
 constexpr uint32_t kMemoValid = 1u << 31;
-#ifdef FFB_SIMT_EMUL
-#define FFB_COMPILER_FENCE() __asm__ __volatile__("" ::: "memory")
-#else
-#define FFB_COMPILER_FENCE() asm volatile("" ::: "memory")
-#endif
+struct Memo {
+  uint4* tab;                    // [2 * kMemoSlots] then the long table (uint32 [kLongSlots][16]); NULL: no memo (token walk only)
+  uint32_t* pend;                // [kPendMax][16] queue of this iteration: 14 key words, value, length
+  unsigned int* n_pend;
+};
+// packed key words of s[p, p+len): word i holds bytes 4i..4i+3, zero beyond len
+FFB_D uint32_t key_word(const uint32_t* wp, int sh, int i, int q, uint32_t pm) {
+  if (i > q) return 0u;
+  const uint32_t v = __funnelshift_r(wp[i], wp[i + 1], sh);
+  return i == q ? (v & pm) : v;
+}
 struct MemoKey { uint32_t k0, k1, k2, k3, k4, k5, slot; };
 FFB_D void memo_key(const uint8_t* s, int p, int len, MemoKey& k) {          // 1 <= len <= 24
   const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + (p & ~3));
@@ -340,16 +352,14 @@ FFB_D void memo_key(const uint8_t* s, int p, int len, MemoKey& k) {          // 
   h ^= h >> 15;
   k.slot = (h * 0x2c1b3c6du) >> 24;
 }
-constexpr int kMemoProbes = 8;
 FFB_D uint32_t memo_probe(const uint4* memo, const MemoKey& k) {             // value with kMemoValid set, or 0
   uint32_t sl = k.slot;
 #pragma unroll 1
   for (int pr = 0; pr < kMemoProbes; ++pr) {
     const uint4 e1 = memo[2 * sl + 1];
-    FFB_COMPILER_FENCE();
+    if (!(e1.z & kMemoValid)) break;                   // empty slot: the opcode is not in the table
     const uint4 e0 = memo[2 * sl];
-    if ((e1.z & kMemoValid) && e1.x == k.k4 && e1.y == k.k5 && e0.x == k.k0 && e0.y == k.k1 && e0.z == k.k2 && e0.w == k.k3) return e1.z;
-    if (e1.w == 0u) break;                             // never claimed: the opcode is not in the table
+    if (e1.x == k.k4 && e1.y == k.k5 && e0.x == k.k0 && e0.y == k.k1 && e0.z == k.k2 && e0.w == k.k3) return e1.z;
     sl = (sl + 1u) & (kMemoSlots - 1);
   }
   return 0u;
@@ -357,110 +367,98 @@ FFB_D uint32_t memo_probe(const uint4* memo, const MemoKey& k) {             // 
 FFB_D uint32_t opcode_bits(const OpcodeInfo& oc) {     // the opcode's share of FfbInsRec.meta
   return oc.cls | (oc.space << 4) | ((oc.bytes & 63u) << 7) | (oc.base << 13) | (oc.cmp << 23);
 }
-// Opcodes of 25..56 bytes (mma / tex / wmma shapes) have a table of their own: 64-byte entries
-// {14 key words, value, state}, same protocol.  Longer ones always take the token walk.
-constexpr int kLongSlots = 32, kLongProbes = 4, kLongWords = 14;
-FFB_NOINLINE uint32_t cold_long_opcode(const uint64_t* tok_key, const uint32_t* tok_val, const uint8_t* s, int p0, int p1, uint32_t* lmemo) {
+FFB_D uint32_t long_hash(const uint32_t* wp, int sh, int q, uint32_t pm) {
+  uint32_t h = 0x811c9dc5u;
+#pragma unroll 1
+  for (int i = 0; i <= q && i < kLongWords; ++i) h = (h ^ key_word(wp, sh, i, q, pm)) * 0x01000193u;
+  h ^= h >> 15;
+  return (h * 0x2c1b3c6du) >> 27;
+}
+// miss (or an opcode of 25..56 bytes): probe the long table if that is where it belongs, else the token walk of the
+// exact kernel; the result is queued for the next insert phase
+FFB_NOINLINE uint32_t cold_opcode(const uint64_t* tok_key, const uint32_t* tok_val, const uint8_t* s, int p0, int p1, const uint32_t* lmemo,
+                                  uint32_t* pend, unsigned int* n_pend) {
   TokTable tt;
   tt.key = tok_key; tt.val = tok_val;
   const int len = p1 - p0;
-  if (len > 4 * kLongWords) return opcode_bits(classify_opcode(tt, s, p0, p1)) | kMemoValid;
   const uint32_t* wp = reinterpret_cast<const uint32_t*>(s + (p0 & ~3));
   const int sh = (p0 & 3) * 8, q = len >> 2;
   const uint32_t pm = (1u << ((len & 3) * 8)) - 1u;
-  uint32_t h = 0x811c9dc5u;
+  if (lmemo && len > 24 && len <= 4 * kLongWords) {
+    uint32_t sl = long_hash(wp, sh, q, pm);
 #pragma unroll 1
-  for (int i = 0; i <= q && i < kLongWords; ++i) {
-    uint32_t v = __funnelshift_r(wp[i], wp[i + 1], sh);
-    if (i == q) v &= pm;
-    h = (h ^ v) * 0x01000193u;
-  }
-  h ^= h >> 15;
-  uint32_t sl = (h * 0x2c1b3c6du) >> 27;
-#pragma unroll 1
-  for (int pr = 0; pr < kLongProbes; ++pr) {
-    uint32_t* e = lmemo + 16 * sl;
-    const uint32_t val = e[14];
-    FFB_COMPILER_FENCE();
-    if (val & kMemoValid) {
+    for (int pr = 0; pr < kLongProbes; ++pr) {
+      const uint32_t* e = lmemo + 16 * sl;
+      const uint32_t val = e[14];
+      if (!(val & kMemoValid)) break;
       bool same = true;
 #pragma unroll 1
-      for (int i = 0; i < kLongWords && same; ++i) {
-        uint32_t v = i <= q ? __funnelshift_r(wp[i < q ? i : q], wp[(i < q ? i : q) + 1], sh) : 0u;
-        if (i == q) v &= pm;
-        same = e[i] == v;
-      }
+      for (int i = 0; i < kLongWords && same; ++i) same = e[i] == key_word(wp, sh, i, q, pm);
       if (same) return val;
-    } else if (e[15] == 0u) break;
-    sl = (sl + 1u) & (kLongSlots - 1);
+      sl = (sl + 1u) & (kLongSlots - 1);
+    }
   }
   const uint32_t val = opcode_bits(classify_opcode(tt, s, p0, p1)) | kMemoValid;
-  sl = (h * 0x2c1b3c6du) >> 27;
-  for (int pr = 0; pr < kLongProbes; ++pr) {
-    uint32_t* e = lmemo + 16 * sl;
-    if (atomicCAS(e + 15, 0u, 1u) == 0u) {
-      for (int i = 0; i < kLongWords; ++i) {
-        uint32_t v = i <= q ? __funnelshift_r(wp[i < q ? i : q], wp[(i < q ? i : q) + 1], sh) : 0u;
-        if (i == q) v &= pm;
-        e[i] = v;
-      }
-      __threadfence_block();
-      e[14] = val;
-      break;
+  if (pend && len <= 4 * kLongWords) {
+    const unsigned int at = atomicAdd(n_pend, 1u);
+    if (at < (unsigned int)kPendMax) {
+      uint32_t* e = pend + 16 * at;
+#pragma unroll 1
+      for (int i = 0; i < kLongWords; ++i) e[i] = key_word(wp, sh, i, q, pm);
+      e[14] = val; e[15] = (uint32_t)len;
     }
-    const uint32_t seen = e[14];
-    FFB_COMPILER_FENCE();
-    if (!(seen & kMemoValid)) break;                   // being written: leave the insert to a later statement
-    bool same = true;
-    for (int i = 0; i < kLongWords && same; ++i) {
-      uint32_t v = i <= q ? __funnelshift_r(wp[i < q ? i : q], wp[(i < q ? i : q) + 1], sh) : 0u;
-      if (i == q) v &= pm;
-      same = e[i] == v;
-    }
-    if (same) break;
-    sl = (sl + 1u) & (kLongSlots - 1);
   }
   return val;
 }
-// memo miss: the token walk of the exact kernel, then the insert
-FFB_NOINLINE uint32_t cold_opcode(const uint64_t* tok_key, const uint32_t* tok_val, const uint8_t* s, int p0, int p1, uint4* memo,
-                                  uint32_t k0, uint32_t k1, uint32_t k2, uint32_t k3, uint32_t k4, uint32_t k5, uint32_t slot) {
-  TokTable tt;
-  tt.key = tok_key; tt.val = tok_val;
-  const uint32_t val = opcode_bits(classify_opcode(tt, s, p0, p1)) | kMemoValid;
-  uint32_t sl = slot;
-  for (int pr = 0; pr < kMemoProbes; ++pr) {
-    uint32_t* state = reinterpret_cast<uint32_t*>(memo + 2 * sl + 1) + 3;
-    if (atomicCAS(state, 0u, 1u) == 0u) {
-      memo[2 * sl] = make_uint4(k0, k1, k2, k3);
-      __threadfence_block();
-      memo[2 * sl + 1] = make_uint4(k4, k5, val, 1u);
-      break;
+// insert phase (one lane, between two CTA barriers): the queued opcodes enter their table unless already there
+FFB_NOINLINE void memo_apply(uint4* tab, const uint32_t* pend, unsigned int n) {
+  uint32_t* lmemo = reinterpret_cast<uint32_t*>(tab + 2 * kMemoSlots);
+  for (unsigned int j = 0; j < n && j < (unsigned int)kPendMax; ++j) {
+    const uint32_t* e = pend + 16 * j;
+    const uint32_t val = e[14], len = e[15];
+    if (len <= 24u) {
+      uint32_t h = (e[0] * 0x9e3779b1u) ^ (e[1] * 0x85ebca77u) ^ (e[2] * 0xc2b2ae3du) ^ (e[3] * 0x27d4eb2fu) ^ (e[4] * 0x165667b1u) ^ (e[5] * 0xd3a2646du);
+      h ^= h >> 15;
+      uint32_t sl = (h * 0x2c1b3c6du) >> 24;
+      for (int pr = 0; pr < kMemoProbes; ++pr) {
+        const uint4 e1 = tab[2 * sl + 1], e0 = tab[2 * sl];
+        if (!(e1.z & kMemoValid)) { tab[2 * sl] = make_uint4(e[0], e[1], e[2], e[3]); tab[2 * sl + 1] = make_uint4(e[4], e[5], val, 1u); break; }
+        if (e1.x == e[4] && e1.y == e[5] && e0.x == e[0] && e0.y == e[1] && e0.z == e[2] && e0.w == e[3]) break;
+        sl = (sl + 1u) & (kMemoSlots - 1);
+      }
+    } else {
+      uint32_t h = 0x811c9dc5u;
+      const int q = (int)(len >> 2);
+      for (int i = 0; i <= q && i < kLongWords; ++i) h = (h ^ e[i]) * 0x01000193u;
+      h ^= h >> 15;
+      uint32_t sl = (h * 0x2c1b3c6du) >> 27;
+      for (int pr = 0; pr < kLongProbes; ++pr) {
+        uint32_t* d = lmemo + 16 * sl;
+        if (!(d[14] & kMemoValid)) { for (int i = 0; i < kLongWords; ++i) d[i] = e[i]; d[14] = val; d[15] = len; break; }
+        bool same = true;
+        for (int i = 0; i < kLongWords && same; ++i) same = d[i] == e[i];
+        if (same) break;
+        sl = (sl + 1u) & (kLongSlots - 1);
+      }
     }
-    // claimed by another lane: while its entry is still being written (most likely this very opcode, missed by
-    // many lanes at once) leave the insert to a later statement; a finished entry with this key ends the search
-    const uint4 e1 = memo[2 * sl + 1];
-    FFB_COMPILER_FENCE();
-    const uint4 e0 = memo[2 * sl];
-    if (!(e1.z & kMemoValid)) break;
-    if (e1.x == k4 && e1.y == k5 && e0.x == k0 && e0.y == k1 && e0.z == k2 && e0.w == k3) break;
-    sl = (sl + 1u) & (kMemoSlots - 1);
   }
-  return val;
 }
 // opcode s[p0, p1) -> opcode bits of the meta word
-FFB_D uint32_t opcode_of(const TokTable& tok, uint4* memo, const uint8_t* s, int p0, int p1) {
+FFB_D uint32_t opcode_of(const TokTable& tok, const Memo& memo, const uint8_t* s, int p0, int p1) {
   const int len = p1 - p0;
-  if (len > 24) return cold_long_opcode(tok.key, tok.val, s, p0, p1, reinterpret_cast<uint32_t*>(memo + 2 * kMemoSlots)) & ~kMemoValid;
-  MemoKey k;
-  memo_key(s, p0, len, k);
-  uint32_t val = memo_probe(memo, k);
-  if (!val) val = cold_opcode(tok.key, tok.val, s, p0, p1, memo, k.k0, k.k1, k.k2, k.k3, k.k4, k.k5, k.slot);
+  uint32_t val = 0;
+  if (memo.tab && len <= 24) {
+    MemoKey k;
+    memo_key(s, p0, len, k);
+    val = memo_probe(memo.tab, k);
+  }
+  if (!val) val = cold_opcode(tok.key, tok.val, s, p0, p1, memo.tab ? reinterpret_cast<const uint32_t*>(memo.tab + 2 * kMemoSlots) : nullptr,
+                              memo.pend, memo.n_pend);
   return val & ~kMemoValid;
 }
 
 template <int kMode>
-FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, uint4* memo, int kb, int ke, Emit& em) {
+FFB_D bool fast_statement(const uint8_t* s, const uint4* MA, const uint4* MB, const Memo& memo, int kb, int ke, Emit& em) {
   const int n = ke - kb;
   const int w0 = kb >> 5, sh = kb & 31;
   const uint64_t valid = low_mask(n);
@@ -755,6 +753,8 @@ lex_fast_kernel(LexArgs a) {
   __shared__ uint64_t s_tok_key[256];
   __shared__ uint32_t s_tok_val[256];
   __shared__ uint4 s_memo[2 * kMemoSlots + 4 * kLongSlots];     // short-opcode table, then the long-opcode table
+  __shared__ uint32_t s_pend[2][kPendMax * 16];                 // opcodes queued for the next insert phase (alternating)
+  __shared__ unsigned int s_npend[2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   uint8_t* s = smem_raw + (size_t)wid * (kRecords ? kFWarpSmemRec : kFWarpSmemHist);
@@ -767,6 +767,7 @@ lex_fast_kernel(LexArgs a) {
   uint32_t* linfo = reinterpret_cast<uint32_t*>(s + kFOffInfo);
   for (int c = threadIdx.x; c < 256; c += (int)blockDim.x) { s_cls[c] = char_class((unsigned)c); s_tok_key[c] = ~0ull; s_tok_val[c] = 0; }
   for (int c = threadIdx.x; c < 2 * kMemoSlots + 4 * kLongSlots; c += (int)blockDim.x) s_memo[c] = make_uint4(0u, 0u, 0u, 0u);
+  if (threadIdx.x < 2) s_npend[threadIdx.x] = 0u;
   __syncthreads();
   for (int c = threadIdx.x; c < kNumTokDefs; c += (int)blockDim.x) {
     const uint32_t slot = (uint32_t)((kTokDefs[c].key * kTokMul) >> 56);
@@ -781,6 +782,7 @@ lex_fast_kernel(LexArgs a) {
 
   // one segment in flight per warp; the loop below handles ONE tile per trip
   bool have = false, done = false, reject = false;
+  int iter = 0;                                                    // trips of the tile loop: the same number in every thread of the CTA
   int64_t seg = 0, seg_begin = 0, seg_end = 0, cur = 0, scan_from_g = 0, body_pos_g = 0;
   int64_t name_off = 0, name_len = 0, body_end_off = 0, ins_base = 0, lab_base = 0;
   int phase = PH_SEARCH, depth = 0;
@@ -812,8 +814,25 @@ lex_fast_kernel(LexArgs a) {
         em.c0 = em.c1 = em.c2 = 0; em.shared_bytes = 0; em.regs = 0;
       }
     }
-    if (kLockstep) { if (!__syncthreads_or(done ? 0 : 1)) break; }
+    if (kLockstep) {
+      if (!__syncthreads_or(done ? 0 : 1)) break;
+      if (kRecords) {
+        // insert phase of the opcode memo: what the previous iteration queued (nobody writes that queue now)
+        const int prev = (iter & 1) ^ 1;
+        const unsigned int np = s_npend[prev];
+        if (np) {
+          if (threadIdx.x == 0) memo_apply(s_memo, s_pend[prev], np);
+          __syncthreads();
+          if (threadIdx.x == 0) s_npend[prev] = 0u;              // every thread has read the count; the queue refills after the NEXT barrier
+        }
+      }
+    }
     else if (done) break;
+    Memo memo;
+    memo.tab = (kRecords && kLockstep) ? s_memo : nullptr;
+    memo.pend = (kRecords && kLockstep) ? s_pend[iter & 1] : nullptr;
+    memo.n_pend = &s_npend[iter & 1];
+    ++iter;
     if (done) continue;                                          // idle warps keep meeting the barrier
 
     if (cur < seg_end) do {
@@ -1112,7 +1131,7 @@ lex_fast_kernel(LexArgs a) {
           if (kind == FK_STMT) {
             em.ins_at = my_ins;
             em.line = line_no + (uint32_t)li;
-            slow = !fast_statement<kMain>(s, MA, MB, s_memo, kb, ke, em);
+            slow = !fast_statement<kMain>(s, MA, MB, memo, kb, ke, em);
           }
           const unsigned slm = __ballot_sync(kFull, slow);
           if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)(li | ((int)(my_ins - ins_base - tile_ins0) << 8));
@@ -1170,7 +1189,7 @@ lex_fast_kernel(LexArgs a) {
           const uint32_t inf = linfo[li];
           em.ins_at = ins_base + tile_ins0 + (ent >> 8);
           em.line = line_no + (uint32_t)li;
-          slow = !fast_statement<kMain>(s, MA, MB, s_memo, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
+          slow = !fast_statement<kMain>(s, MA, MB, memo, (int)(inf & 0x1fffu), (int)((inf >> 13) & 0x1fffu), em);
         }
         const unsigned slm = __ballot_sync(kFull, slow);
         if (slow) slist[n_slow + __popc(slm & lt_mask)] = (uint16_t)ent;
