@@ -44,6 +44,10 @@ def parse_args():
     ap.add_argument("--corpus-mb", type=int, default=-1, help="PTX shard per rank in MB (-1: 1250 when the lexer is built)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunk-mb", type=int, default=384, help="chunk size of the overlapped host->device pipeline of the e2e leg")
+    ap.add_argument("--e2e-head-mb", type=int, default=0, help="size of the first upload chunk (0: a full chunk)")
+    ap.add_argument("--e2e-tail-mb", type=int, default=0, help="the last chunks halve down to this size (0: full chunks to the end)")
+    ap.add_argument("--e2e-pipelines", type=int, default=1, help="compute streams (each with its own libffb context) the chunks alternate between")
+    ap.add_argument("--e2e-sweep", type=str, default="", help="extra e2e timings, 'chunk:head:tail:pipelines' settings separated by commas (MB)")
     ap.add_argument("--lex-flags", type=int, default=0, help="FFB_LEX_* bits for A/B runs (2 = no lock-step CTAs)")
     ap.add_argument("--unfused", action="store_true", help="score + front as two kernels with the [K,S,J,C] grid in HBM "
                     "(ffb_predict_grid -> ffb_skyline_groups) instead of the fused ffb_explore_groups")
@@ -171,7 +175,8 @@ def main():
     bufs = {"t": torch.empty((K, 1, J, C), dtype=torch.float64, device=dev),
             "e": torch.empty((K, 1, J, C), dtype=torch.float64, device=dev)}
     if corpus is not None:
-        lex_state = corpus_mod.BenchLexState(rt, corpus, chunk_bytes=args.e2e_chunk_mb << 20)
+        lex_state = corpus_mod.BenchLexState(rt, corpus, chunk_bytes=args.e2e_chunk_mb << 20, pipelines=args.e2e_pipelines,
+                                             head_bytes=args.e2e_head_mb << 20, tail_bytes=args.e2e_tail_mb << 20)
 
     # size the compact front buffer from one untimed, checked pass (inputs are the same every step)
     feat0 = lex_state.run(resident=True) if corpus is not None else d_feat
@@ -216,7 +221,8 @@ def main():
         side.wait_stream(main)
         fn, tp, fo = front_bufs[1], front_bufs[2], front_bufs[3]
 
-        def on_chunk(c, s0, s1):
+        def on_chunk(c, s0, s1, rt):                              # rt: the runtime of the chunk's compute stream
+            main = torch.cuda.current_stream(dev)
             lo, hi = e2e["regions"][c]
             if args.unfused:
                 r = engine.score_grid(lex_state.feat[s0:s1], res[s0:s1], sp, shp, CAPS, want=("t", "e"),
@@ -313,6 +319,21 @@ def main():
         sampler.start()
     ms_dev, phase_ms, launches = run(True, args.steps, args.warmup)
     clocks = sampler.stop() if rank == 0 else None
+    # optional: the e2e step under other chunk schedules / pipeline counts (reported as e2e.sweep_ms)
+    e2e_sweep = {}
+    if corpus is not None and args.e2e_sweep:
+        for setting in args.e2e_sweep.split(","):
+            chunk, head, tail, pipes = (int(x) for x in setting.split(":"))
+            lex_state.chunk_bytes, lex_state.head_bytes, lex_state.tail_bytes, lex_state.pipelines = chunk << 20, head << 20, tail << 20, pipes
+            lex_state.streamed, e2e["regions"] = None, None
+            ms_s, _, _ = run(False, 4, 2)
+            torch.cuda.synchronize()
+            assert np.array_equal(h_front_n.numpy().astype(np.int64), fn0_host), f"e2e sweep {setting}: front sizes differ"
+            e2e_sweep[setting] = {"ms_per_step": round(ms_s / 4, 3), "chunks": len(lex_state.streamed.bounds)}
+            print(f"[e2e sweep] {setting}: {ms_s / 4:.2f} ms, {len(lex_state.streamed.bounds)} chunks", file=sys.stderr, flush=True)
+        lex_state.chunk_bytes, lex_state.head_bytes, lex_state.tail_bytes, lex_state.pipelines = (
+            args.e2e_chunk_mb << 20, args.e2e_head_mb << 20, args.e2e_tail_mb << 20, args.e2e_pipelines)
+        lex_state.streamed, e2e["regions"] = None, None
     ms_e2e, _, _ = run(False, max(3, args.steps // 2), 2)
     e2e_steps = max(3, args.steps // 2)
     # one more streamed step with timing events on both streams: where the step's time goes (ms since its start)
@@ -545,10 +566,10 @@ def main():
                 "h2d_bytes_per_step": int(h_feat.numel() * 8 + h_res.numel() * 8 + lex_bytes_rank) * world,
                 "d2h_bytes_per_step": int((e2e["h_front"].numel() if e2e.get("h_front") is not None else h_front.numel()) * 4
                                           + h_front_n.numel() * 4 + h_front_off.numel() * 8) * world,
-                "pipeline": (f"{len(e2e['regions'])} chunks of <= {args.e2e_chunk_mb} MB: upload, K1+K1b, K2+K3, K4 and the front read-back overlap"
+                "pipeline": (f"{len(e2e['regions'])} chunks of <= {args.e2e_chunk_mb} MB (first {args.e2e_head_mb or args.e2e_chunk_mb} MB, last ones halving down to {args.e2e_tail_mb or args.e2e_chunk_mb} MB) alternating between {args.e2e_pipelines} compute stream(s): upload, K1+K1b, K2+K3+K4 and the front read-back overlap"
                              if e2e.get("regions") else "none"),
                 "ms_per_step": ms_e2e / e2e_steps, "steps": e2e_steps, "h2d_alone_ms": h2d_alone_ms,
-                "timeline_ms": e2e_timeline},
+                "timeline_ms": e2e_timeline, **({"sweep_ms": e2e_sweep} if e2e_sweep else {})},
         "roofline": roofline, "cpu_baseline": cpu,
     }
     print(json.dumps(out))

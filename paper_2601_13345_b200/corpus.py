@@ -6,6 +6,8 @@ A corpus is one byte buffer plus a segment table; segment k is analysed exactly 
 """
 from __future__ import annotations
 
+import contextlib
+
 import ctypes as C
 from dataclasses import dataclass
 
@@ -406,23 +408,49 @@ def replicated_corpus(unit: bytes, unit_off: np.ndarray, target_bytes: int, rt: 
                   order=order, host_text=unit, host_off=unit_off)
 
 
+def chunk_schedule(total: int, chunk_bytes: int, head_bytes: int = 0, tail_bytes: int = 0) -> list[int]:
+    """Target sizes of the upload chunks: an optional small first chunk (the kernels start ``head_bytes`` into the
+    upload instead of ``chunk_bytes``), full chunks, then - when ``tail_bytes`` > 0 - chunks that halve down to
+    ``tail_bytes``, so that little work is left when the last byte arrives."""
+    sizes, left = [], int(total)
+    if 0 < head_bytes < left:
+        sizes.append(int(head_bytes))
+        left -= int(head_bytes)
+    while left > 0:
+        if tail_bytes > 0:
+            size = left if left <= tail_bytes * 3 // 2 else min(chunk_bytes, max(tail_bytes, left // 2))
+        else:
+            size = min(chunk_bytes, left)
+        sizes.append(int(size))
+        left -= int(size)
+    return sizes
+
+
 class StreamedAnalysis:
     """text in PINNED HOST memory -> feature rows, with the host->device copy overlapped with the
-    kernels: the corpus is cut at segment boundaries into chunks of about ``chunk_bytes``; a copy
-    stream uploads chunk c+1 while the compute stream runs K1 (single-pass record mode) and K1b on
-    chunk c.  Results are identical to ``analyze_corpus`` on the resident text."""
+    kernels: the corpus is cut at segment boundaries into chunks (``chunk_schedule``); a copy
+    stream uploads chunk c+1 while chunk c runs K1 (single-pass record mode) and K1b.  With
+    ``pipelines`` > 1 the chunks alternate between that many compute streams, each with its own
+    libffb context (scratch, work queues): every launch ends with a few long kernels on one warp
+    each, and the next chunk's launches fill the SMs those tails leave idle.  Results are
+    identical to ``analyze_corpus`` on the resident text."""
 
     def __init__(self, rt: native.Runtime, corp: Corpus, host_text: torch.Tensor, *, chunk_bytes: int = 384 << 20,
-                 lex: LexResult | None = None, feat: torch.Tensor | None = None):
+                 lex: LexResult | None = None, feat: torch.Tensor | None = None, pipelines: int = 1,
+                 head_bytes: int = 0, tail_bytes: int = 0):
         assert host_text.is_pinned() and host_text.numel() == corp.padded_bytes
         self.rt, self.corp, self.host = rt, corp, host_text
         seg = corp.seg_off.cpu().numpy()
         bounds, s0 = [], 0
-        while s0 < corp.n_segs:
-            s1 = int(np.searchsorted(seg, seg[s0] + chunk_bytes, side="left"))
+        for size in chunk_schedule(int(seg[-1]), chunk_bytes, head_bytes, tail_bytes):
+            if s0 >= corp.n_segs:
+                break
+            s1 = int(np.searchsorted(seg, seg[s0] + size, side="left"))
             s1 = min(max(s1, s0 + 1), corp.n_segs)
             bounds.append((s0, s1))
             s0 = s1
+        if s0 < corp.n_segs:
+            bounds.append((s0, corp.n_segs))
         self.bounds = bounds
         # copy ranges: 16-byte aligned supersets of the chunks' bytes (neighbouring bytes are re-sent, harmless)
         self.ranges = [(int(seg[a]) // 16 * 16, min((int(seg[b]) + 15) // 16 * 16 + 16, corp.padded_bytes)) for a, b in bounds]
@@ -431,12 +459,20 @@ class StreamedAnalysis:
         self.lex = lex if lex is not None else lex_records_single_pass(corp, rt=rt)
         self.feat = feat if feat is not None else rt.empty((corp.n_segs, native.FEAT_WIDTH), torch.float64)
         self.status = rt.empty((corp.n_segs,), torch.int32)
-        self.copy_stream = torch.cuda.Stream(device=rt.device) if rt.device.type == "cuda" else None
-        self.events = [torch.cuda.Event() for _ in bounds] if self.copy_stream is not None else []
+        cuda = rt.device.type == "cuda"
+        self.copy_stream = torch.cuda.Stream(device=rt.device) if cuda else None
+        self.events = [torch.cuda.Event() for _ in bounds] if cuda else []
+        # compute pipelines: (runtime, stream); pipeline 0 is the caller's runtime on the caller's stream
+        self.pipes = [(rt, None)]
+        if cuda:
+            for _ in range(1, max(1, int(pipelines))):
+                self.pipes.append((native.Runtime(native.load_library(), rt.device, rt.device.index or 0),
+                                   torch.cuda.Stream(device=rt.device)))
 
     def run(self, default_trip: float = 32.0, on_chunk=None, timeline: list | None = None) -> torch.Tensor:
-        """``on_chunk(c, s0, s1)`` runs on the compute stream right after chunk c's feature rows are
-        enqueued (e.g. to score and rank those kernels while later chunks are still uploading).
+        """``on_chunk(c, s0, s1, rt)`` runs on the chunk's compute stream (the current stream during the
+        call) right after chunk c's feature rows are enqueued, with the runtime whose scratch that
+        stream owns (e.g. to score and rank those kernels while later chunks are still uploading).
         ``timeline``: when a list, timing events are appended as (label, event) - one after every chunk's
         upload (copy stream) and after its lexer / dataflow / on_chunk work (compute stream)."""
         rt, corp = self.rt, self.corp
@@ -447,10 +483,13 @@ class StreamedAnalysis:
                 ev.record(stream if stream is not None else torch.cuda.current_stream(rt.device))
                 timeline.append((label, ev))
 
+        main = None
         if self.copy_stream is not None:
             main = torch.cuda.current_stream(rt.device)
             mark("start")
             self.copy_stream.wait_stream(main)            # earlier readers of the text buffer are done
+            for _, st in self.pipes[1:]:
+                st.wait_stream(main)
             with torch.cuda.stream(self.copy_stream):
                 for c, ((lo, hi), ev) in enumerate(zip(self.ranges, self.events)):
                     corp.text[lo:hi].copy_(self.host[lo:hi], non_blocking=True)
@@ -459,16 +498,20 @@ class StreamedAnalysis:
         else:
             corp.text.copy_(self.host)
         for c, (s0, s1) in enumerate(self.bounds):
-            if self.copy_stream is not None:
-                torch.cuda.current_stream(rt.device).wait_event(self.events[c])
-            lex_records_single_pass(corp, out=self.lex, rt=rt, seg_range=(s0, s1), order=self.orders[c])
-            mark(f"lex[{c}]")
-            kernel_features(corp, self.lex, default_trip=default_trip, out_feat=self.feat, out_status=self.status, rt=rt,
-                            seg_range=(s0, s1), order=self.orders[c])
-            mark(f"flow[{c}]")
-            if on_chunk is not None:
-                on_chunk(c, s0, s1)
-                mark(f"score+front[{c}]")
+            rt_c, st = self.pipes[c % len(self.pipes)]
+            with (torch.cuda.stream(st) if st is not None else contextlib.nullcontext()):
+                if self.copy_stream is not None:
+                    torch.cuda.current_stream(rt.device).wait_event(self.events[c])
+                lex_records_single_pass(corp, out=self.lex, rt=rt_c, seg_range=(s0, s1), order=self.orders[c])
+                mark(f"lex[{c}]")
+                kernel_features(corp, self.lex, default_trip=default_trip, out_feat=self.feat, out_status=self.status, rt=rt_c,
+                                seg_range=(s0, s1), order=self.orders[c])
+                mark(f"flow[{c}]")
+                if on_chunk is not None:
+                    on_chunk(c, s0, s1, rt_c)
+                    mark(f"score+front[{c}]")
+        for _, st in self.pipes[1:]:
+            main.wait_stream(st)                          # the caller's stream sees every chunk's results
         return self.feat
 
 
@@ -477,8 +520,10 @@ class BenchLexState:
     single-pass record mode (slots sized from the segment lengths, nothing is learnt from a
     previous pass over the same text) followed by the dataflow kernel."""
 
-    def __init__(self, rt: native.Runtime, corp: Corpus, chunk_bytes: int = 384 << 20):
+    def __init__(self, rt: native.Runtime, corp: Corpus, chunk_bytes: int = 384 << 20, pipelines: int = 1,
+                 head_bytes: int = 0, tail_bytes: int = 0):
         self.rt, self.corp, self.chunk_bytes = rt, corp, chunk_bytes
+        self.pipelines, self.head_bytes, self.tail_bytes = pipelines, head_bytes, tail_bytes
         self.lex = lex_records_single_pass(corp, rt=rt)
         self.feat = rt.empty((corp.n_segs, native.FEAT_WIDTH), torch.float64)
         self.host_text = None
@@ -496,7 +541,8 @@ class BenchLexState:
             # host text -> feature rows through the public streamed path: H2D inside the timed
             # region, overlapped chunk by chunk with K1 / K1b
             if self.streamed is None:
-                self.streamed = StreamedAnalysis(rt, corp, self.pin_host(), lex=self.lex, feat=self.feat, chunk_bytes=self.chunk_bytes)
+                self.streamed = StreamedAnalysis(rt, corp, self.pin_host(), lex=self.lex, feat=self.feat, chunk_bytes=self.chunk_bytes,
+                                                 pipelines=self.pipelines, head_bytes=self.head_bytes, tail_bytes=self.tail_bytes)
             self.streamed.run(on_chunk=on_chunk, timeline=timeline)
             if mark is not None:
                 mark.record()

@@ -188,16 +188,23 @@ predict_grid_kernel(GridArgs a) {
 
 // The streaming configuration (t / e only) with the factored model of ffb_model.cuh: one CTA per (kernel, spec)
 // group evaluates the group's class rows once - (threads, regs) classes and clipped-block_x classes - and then
-// walks the group's shapes 256 at a time: two fp64 divides per shape instead of ten (round 1: 780 thread
-// instructions per unit, 44% of the copy peak).  Same staging and coalesced write-out as predict_grid_kernel.
+// walks the group's shapes: two fp64 divides per shape instead of ten (round 1: 780 thread instructions per unit,
+// 44% of the copy peak).  Same staging tile and coalesced write-out as predict_grid_kernel, in CTAs of 128 shapes
+// (eight resident per SM: the stores of one overlap the fp64 chains of the others); the cap table of the group's
+// spec sits in shared memory.  Measured and rejected (r2x): no staging tile - every lane owns elements L, L + 32, ...
+// of the warp's 32 x C outputs and fetches (t_exec, p_pre) of the element's shape with shuffles - 57% more warp
+// instructions (shuffles, divergent cap-table reads, 8-byte stores), 0.49 ms vs 0.44 ms.
 constexpr int kGridMaxClassA = 512;
-__global__ void __launch_bounds__(kUnitsPerCta, 4)
+constexpr int kClsSpan = 512;                  // shapes per CTA (a multiple of kClsUnits)
+constexpr int kClsUnits = 128;                 // threads per CTA = shapes per pass (four warps of 32 shapes)
+__global__ void __launch_bounds__(kClsUnits, 8)
 predict_grid_classes_kernel(GridArgs a) {
   FFB_DYN_SMEM(smem_raw);
   const int C = a.n_caps, J = a.n_shapes;
-  double* s_t = reinterpret_cast<double*>(smem_raw);            // [units][C]
-  double* s_e = s_t + (size_t)kUnitsPerCta * C;
-  double* s_ca = s_e + (size_t)kUnitsPerCta * C;                // [n_a][kClassAWidth]
+  double* s_t = reinterpret_cast<double*>(smem_raw);            // [units][C] staging tile
+  double* s_e = s_t + (size_t)kClsUnits * C;
+  double* s_cap = s_e + (size_t)kClsUnits * C;                  // [C][4] = {scale, cap, room, ok} of this spec
+  double* s_ca = s_cap + (size_t)C * 4;                         // [n_a][kClassAWidth]
   double* s_cb = s_ca + (size_t)a.tb.n_a * kClassAWidth;        // [n_b][kClassBWidth]
   const int64_t g = blockIdx.x;
   const int64_t k = g / a.n_specs;
@@ -209,18 +216,22 @@ predict_grid_classes_kernel(GridArgs a) {
   const int64_t shared_dyn = a.res[2 * k + 0], total_blocks = a.res[2 * k + 1];
   const bool classes = f[FFB_F_OVR] == 0.0;
   if (classes) {
-    for (int i = threadIdx.x; i < a.tb.n_a + a.tb.n_b; i += kUnitsPerCta) {
+    for (int i = threadIdx.x; i < a.tb.n_a + a.tb.n_b; i += kClsUnits) {
       if (i < a.tb.n_a) eval_class_a(f, sp, sd, kr, a.tb.a_rep[2 * i], a.tb.a_rep[2 * i + 1], shared_dyn, total_blocks, s_ca + (size_t)i * kClassAWidth);
       else eval_class_b(f, sp, sd, a.tb.b_rep[i - a.tb.n_a], s_cb + (size_t)(i - a.tb.n_a) * kClassBWidth);
     }
   }
+  for (int i = threadIdx.x; i < C * 4; i += kClsUnits) s_cap[i] = a.tb.cap_tab[(size_t)s * C * 4 + i];
   __syncthreads();
   const double p_static = sp[FFB_S_P_STATIC], e_over = sp[FFB_S_E_OVERHEAD];
-  const double2* ct2 = reinterpret_cast<const double2*>(a.tb.cap_tab + (size_t)s * C * 4);
-  for (int j0 = 0; j0 < J; j0 += kUnitsPerCta) {
+  const double2* s_cap2 = reinterpret_cast<const double2*>(s_cap);
+  // blockIdx.y: this CTA's run of kClsSpan shapes (large shape tables are split so that the grid has many more
+  // CTAs than the GPU holds at once: no tail of half-empty waves)
+  const int j_begin = (int)blockIdx.y * kClsSpan, j_end = j_begin + kClsSpan < J ? j_begin + kClsSpan : J;
+  for (int j0 = j_begin; j0 < j_end; j0 += kClsUnits) {
     const int j = j0 + threadIdx.x;
-    const int n_live = J - j0 < kUnitsPerCta ? J - j0 : kUnitsPerCta;
-    if (j < J) {
+    const int n_live = j_end - j0 < kClsUnits ? j_end - j0 : kClsUnits;
+    if (j < j_end) {
       double t_exec, p_pre;
       bool valid;
       if (classes) {
@@ -233,15 +244,17 @@ predict_grid_classes_kernel(GridArgs a) {
         eval_unit(f, sp, sd, kr, a.tb.shape + 4 * j, a.tb.shape_log[j], shared_dyn, total_blocks, 0, u);
         t_exec = u.t_exec; p_pre = u.p_pre; valid = u.valid;
       }
+      double* st = s_t + (size_t)threadIdx.x * C;
+      double* se = s_e + (size_t)threadIdx.x * C;
+#pragma unroll 4
       for (int c = 0; c < C; ++c) {
-        const double2 sc_cap = ct2[2 * c], room_ok = ct2[2 * c + 1];
+        const double2 sc_cap = s_cap2[2 * c], room_ok = s_cap2[2 * c + 1];   // same address in every lane: broadcast
         double p_dyn;
         bool limited;
         const double e_pred = eval_cap(t_exec, p_pre, p_static, e_over, sc_cap.x, sc_cap.y, room_ok.x, &p_dyn, &limited);
         const bool ok = valid && room_ok.y != 0.0;
-        const size_t o = (size_t)threadIdx.x * C + c;
-        s_t[o] = ok ? t_exec : INFINITY;
-        s_e[o] = ok ? e_pred : INFINITY;
+        st[c] = ok ? t_exec : INFINITY;
+        se[c] = ok ? e_pred : INFINITY;
       }
     }
     __syncthreads();
@@ -253,10 +266,10 @@ predict_grid_classes_kernel(GridArgs a) {
       double2* ge = reinterpret_cast<double2*>(a.e + base);
       const double2* st2 = reinterpret_cast<const double2*>(s_t);
       const double2* se2 = reinterpret_cast<const double2*>(s_e);
-      for (int i = threadIdx.x; i < pairs; i += kUnitsPerCta) { gt[i] = st2[i]; ge[i] = se2[i]; }
+      for (int i = threadIdx.x; i < pairs; i += kClsUnits) { gt[i] = st2[i]; ge[i] = se2[i]; }
       if ((total & 1) && threadIdx.x == 0) { a.t[base + total - 1] = s_t[total - 1]; a.e[base + total - 1] = s_e[total - 1]; }
     } else {
-      for (int i = threadIdx.x; i < total; i += kUnitsPerCta) { a.t[base + i] = s_t[i]; a.e[base + i] = s_e[i]; }
+      for (int i = threadIdx.x; i < total; i += kClsUnits) { a.t[base + i] = s_t[i]; a.e[base + i] = s_e[i]; }
     }
     __syncthreads();
   }
@@ -458,11 +471,11 @@ extern "C" int32_t ffb_predict_grid(FfbContext* ctx, const FfbGridDesc* g, void*
   if (g->d_detail) {
     FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FFB_LAUNCH((predict_grid_kernel<true, false>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);
-  } else if (lean && a.t && a.e && a.cap_tile == (int)C && tb.n_a > 0 && tb.n_a <= kGridMaxClassA && K * S <= 0x7fffffffLL &&
-             smem + ((size_t)tb.n_a * kClassAWidth + (size_t)tb.n_b * kClassBWidth) * sizeof(double) <= 96 * 1024) {
-    const size_t smem_c = (size_t)kUnitsPerCta * C * 16 + ((size_t)tb.n_a * kClassAWidth + (size_t)tb.n_b * kClassBWidth) * sizeof(double);
+  } else if (lean && a.t && a.e && tb.n_a > 0 && tb.n_a <= kGridMaxClassA && K * S <= 0x7fffffffLL && (J + kClsSpan - 1) / kClsSpan <= 65535 &&
+             ((size_t)kClsUnits * C * 2 + (size_t)C * 4 + (size_t)tb.n_a * kClassAWidth + (size_t)tb.n_b * kClassBWidth) * sizeof(double) <= 96 * 1024) {
+    const size_t smem_c = ((size_t)kClsUnits * C * 2 + (size_t)C * 4 + (size_t)tb.n_a * kClassAWidth + (size_t)tb.n_b * kClassBWidth) * sizeof(double);
     FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_classes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
-    FFB_LAUNCH(predict_grid_classes_kernel, (unsigned)(K * S), kUnitsPerCta, smem_c, stream, a);
+    FFB_LAUNCH(predict_grid_classes_kernel, dim3((unsigned)(K * S), (unsigned)((J + kClsSpan - 1) / kClsSpan)), kClsUnits, smem_c, stream, a);
   } else if (lean) {
     FFB_CUDA(ctx, cudaFuncSetAttribute(predict_grid_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FFB_LAUNCH((predict_grid_kernel<false, true>), (unsigned)n_cta, kUnitsPerCta, smem, stream, a);

@@ -342,9 +342,21 @@ def test_segment_range_calls_equal_whole_corpus(backend):
     assert feat.cpu().numpy()[:, :11].tobytes() == fl_all.feat.cpu().numpy()[:, :11].tobytes()
 
 
+def test_chunk_schedule():
+    """Upload schedule of StreamedAnalysis: sizes add up, the head is small, the tail halves down."""
+    assert corpus.chunk_schedule(1000, 384) == [384, 384, 232]
+    assert corpus.chunk_schedule(1389, 384, 0, 64) == [384, 384, 310, 155, 78, 78]
+    assert corpus.chunk_schedule(1389, 384, 96, 0) == [96, 384, 384, 384, 141]
+    for total, chunk, head, tail in [(1, 384, 0, 0), (5000, 100, 30, 7), (50, 384, 96, 64), (97, 96, 96, 0)]:
+        sizes = corpus.chunk_schedule(total, chunk, head, tail)
+        assert sum(sizes) == total and min(sizes) > 0 and max(sizes) <= max(chunk, head)
+
+
 @pytest.mark.gpu
-def test_streamed_analysis_equals_resident(gpu_only):
-    """StreamedAnalysis (pinned host text, copy overlapped with the kernels) == analyze on resident text."""
+@pytest.mark.parametrize("pipelines,head,tail", [(1, 0, 0), (2, 0, 0), (3, 1 << 18, 1 << 17)])
+def test_streamed_analysis_equals_resident(gpu_only, pipelines, head, tail):
+    """StreamedAnalysis (pinned host text, copy overlapped with the kernels; chunks alternating between compute
+    streams with their own contexts; short first / last chunks) == analyze on resident text."""
     import torch
     text, offs = synth.ptx_corpus(seed=33, n_kernels=300, lo=20, hi=3000)
     corp = corpus.upload_corpus(text, offs)
@@ -352,10 +364,14 @@ def test_streamed_analysis_equals_resident(gpu_only):
     host = torch.empty(corp.padded_bytes, dtype=torch.uint8).pin_memory()
     host.copy_(corp.text)
     corp.text.zero_()
-    sa = corpus.StreamedAnalysis(gpu_only, corp, host, chunk_bytes=1 << 20)
-    assert len(sa.bounds) > 3
+    sa = corpus.StreamedAnalysis(gpu_only, corp, host, chunk_bytes=1 << 20, pipelines=pipelines, head_bytes=head, tail_bytes=tail)
+    assert len(sa.bounds) > 3 and len(sa.pipes) == pipelines and sa.bounds[0][0] == 0 and sa.bounds[-1][1] == corp.n_segs
+    assert all(a[1] == b[0] for a, b in zip(sa.bounds, sa.bounds[1:]))
+    seen = []
+    feat = sa.run(on_chunk=lambda c, s0, s1, rt: seen.append((c, s0, s1, rt is sa.pipes[c % pipelines][0])))
     feat = sa.run()
     torch.cuda.synchronize()
+    assert [x[1:3] for x in seen] == sa.bounds and all(x[3] for x in seen)
     assert np.array_equal(sa.status.cpu().numpy(), fl.status.cpu().numpy())
     assert feat.cpu().numpy()[:, :11].tobytes() == fl.feat.cpu().numpy()[:, :11].tobytes()
 
