@@ -46,7 +46,7 @@ def parse_args():
     ap.add_argument("--e2e-chunk-mb", type=int, default=384, help="chunk size of the overlapped host->device pipeline of the e2e leg")
     ap.add_argument("--e2e-head-mb", type=int, default=0, help="size of the first upload chunk (0: a full chunk)")
     ap.add_argument("--e2e-tail-mb", type=int, default=0, help="the last chunks halve down to this size (0: full chunks to the end)")
-    ap.add_argument("--e2e-pipelines", type=int, default=1, help="compute streams (each with its own libffb context) the chunks alternate between")
+    ap.add_argument("--e2e-pipelines", type=int, default=2, help="compute streams (each with its own libffb context) the chunks alternate between")
     ap.add_argument("--e2e-sweep", type=str, default="", help="extra e2e timings, 'chunk:head:tail:pipelines' settings separated by commas (MB)")
     ap.add_argument("--lex-flags", type=int, default=0, help="FFB_LEX_* bits for A/B runs (2 = no lock-step CTAs)")
     ap.add_argument("--unfused", action="store_true", help="score + front as two kernels with the [K,S,J,C] grid in HBM "

@@ -281,8 +281,15 @@ lex_corpus_kernel(LexArgs a) {
         }
       }
       const int n_real = total_nl < kMaxLines ? total_nl : kMaxLines;
+      // A tile without a newline whose last byte lies inside a `//` comment: the staged bytes are the code of one
+      // physical line followed by comment text, and whatever follows up to the real newline is comment as well
+      // (the automaton state is carried into the next tile).  The line is closed at `hi`; the rest of the comment
+      // becomes a blank line that owns the real newline, which ptx.py:230 skips - same statements, same line numbers.
+      const int tile_end_state = __shfl_sync(kFull, st_out, 31);
+      const bool comment_tail = !at_seg_end && total_nl == 0 && hi - lo >= kTile / 2 &&
+                                (tile_end_state == S_LINE || tile_end_state == S_LINE_SLASH || tile_end_state == S_LBLK || tile_end_state == S_LBLK_STAR);
       // the text may end without a newline: close the last line at `hi`
-      const bool virtual_last = at_seg_end && total_nl < kMaxLines;
+      const bool virtual_last = (at_seg_end || comment_tail) && total_nl < kMaxLines;
       if (virtual_last && lane == 0) nl[n_real] = (uint16_t)hi;
       const int n_lines = n_real + (virtual_last ? 1 : 0);
       __syncwarp();
@@ -509,7 +516,7 @@ lex_corpus_kernel(LexArgs a) {
       int nlc = 0;
       for (int l = lane; l < n_real; l += 32) nlc += ((nl[l] & 0x7fff) < consume_to) ? 1 : 0;
       nlc = (int)warp_sum_u64((unsigned long long)nlc);
-      cm_state = S_CODE;
+      cm_state = (comment_tail && consume_to == hi) ? tile_end_state : S_CODE;
       if (nlc > 0) {
         const unsigned last = nl[nlc - 1];
         if ((int)(last & 0x7fff) == consume_to - 1 && (last & 0x8000)) cm_state = S_BLK;

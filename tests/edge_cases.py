@@ -73,4 +73,10 @@ EDGE_CASES = {
         "membar.gl", "cp.async.ca.shared.global", "tcgen05.mma.cta_group::1.kind::f16", "bra.uni",
         "ld.global.v2.v4.f32.f64", "st.shared.global.u16", "setp.lt.and.s32", "mov.b64", "shr.u32", "and.pred"))
         + "\nT: ret;").replace("bra.uni %r1, %r2;", "bra.uni T;"),
+    # `//` comments longer than a 4 KB tile (the lexer closes the line at the tile edge and carries the comment state):
+    # a comment-only line, a comment behind a statement, one spanning three tiles, one holding "/*" and "*/"
+    "long_line_comment": _k("add.s32 %r1, %r2, 1;\n // " + "x" * 5000 + "\n sub.s32 %r1, %r1, 2;\nL: bra L;\n ret;"),
+    "long_trailing_comment": _k("add.s32 %r1, %r2, 1; // " + "y; " * 1700 + "\n @%p1 sub.s32 %r1, %r1, 2; // short\n ret;"),
+    "huge_line_comment": "// " + "z{" * 6500 + "\n" + _k("ld.global.f32 %f1, [%rd1]; //" + "/" * 9000 + "\n st.global.f32 [%rd1], %f1;\n ret;"),
+    "long_comment_with_block_marks": _k("mov.u32 %r1, 1; // " + "a" * 3000 + " /* " + "b" * 3000 + " */ " + "c" * 3000 + "\n mov.u32 %r2, 2;\n ret;"),
 }
