@@ -43,7 +43,7 @@ def parse_args():
     ap.add_argument("--kernels", type=int, default=KERNELS_PER_RANK, help="kernels per rank")
     ap.add_argument("--corpus-mb", type=int, default=-1, help="PTX shard per rank in MB (-1: 1250 when the lexer is built)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-chunk-mb", type=int, default=384, help="chunk size of the overlapped host->device pipeline of the e2e leg")
+    ap.add_argument("--e2e-chunk-mb", type=int, default=192, help="chunk size of the overlapped host->device pipeline of the e2e leg")
     ap.add_argument("--e2e-head-mb", type=int, default=0, help="size of the first upload chunk (0: a full chunk)")
     ap.add_argument("--e2e-tail-mb", type=int, default=0, help="the last chunks halve down to this size (0: full chunks to the end)")
     ap.add_argument("--e2e-pipelines", type=int, default=2, help="compute streams (each with its own libffb context) the chunks alternate between")

@@ -288,13 +288,23 @@ lex_corpus_kernel(LexArgs a) {
       const int tile_end_state = __shfl_sync(kFull, st_out, 31);
       const bool comment_tail = !at_seg_end && total_nl == 0 && hi - lo >= kTile / 2 &&
                                 (tile_end_state == S_LINE || tile_end_state == S_LINE_SLASH || tile_end_state == S_LBLK || tile_end_state == S_LBLK_STAR);
+      // A tile without a newline while the kernel is still being looked for (module-level initialiser lists are
+      // emitted on one line of any length): nothing but `.entry`, the kernel name and the opening brace matter
+      // there (ptx.py:165-176 works on the whole text), so the tile is cut at the last 128-byte chunk edge whose
+      // automaton state needs no look-behind and the next tile resumes there in that state.
+      int cut = -1, cut_state = S_CODE;
+      if (!at_seg_end && total_nl == 0 && !comment_tail && (phase == PH_SEARCH || phase == PH_HEADER)) {
+        const unsigned okm = __ballot_sync(kFull, chunk_base > lo && chunk_base < hi && st_in != S_SLASH && st_in != S_SLASH2);
+        if (okm) { const int l = 31 - __clz((int)okm); cut = l * kLaneBytes; cut_state = __shfl_sync(kFull, st_in, l); }
+      }
+      const int line_hi = cut >= 0 ? cut : hi;
       // the text may end without a newline: close the last line at `hi`
-      const bool virtual_last = (at_seg_end || comment_tail) && total_nl < kMaxLines;
-      if (virtual_last && lane == 0) nl[n_real] = (uint16_t)hi;
+      const bool virtual_last = (at_seg_end || comment_tail || cut >= 0) && total_nl < kMaxLines;
+      if (virtual_last && lane == 0) nl[n_real] = (uint16_t)line_hi;
       const int n_lines = n_real + (virtual_last ? 1 : 0);
       __syncwarp();
       if (n_lines == 0) { status = FFB_E_CAPACITY; break; }         // a line longer than the tile
-      const int region_end = virtual_last ? hi : (nl[n_real - 1] & 0x7fff) + 1;
+      const int region_end = virtual_last ? line_hi : (nl[n_real - 1] & 0x7fff) + 1;
       int consume_to = region_end;     // smem index where the next tile starts
       bool skip_rest = false;
 
@@ -346,6 +356,9 @@ lex_corpus_kernel(LexArgs a) {
           body_pos_g = abase + cand + 1;
         }
       }
+
+      // a cut tile never runs body lines: the body is re-staged from its first byte
+      if (cut >= 0 && phase == PH_BODY && !skip_rest) { skip_rest = true; consume_to = (int)(body_pos_g - abase); }
 
       // ================= T3b: body lines (ptx.py:227-270) =================
       if (phase == PH_BODY && !skip_rest) {
@@ -516,7 +529,7 @@ lex_corpus_kernel(LexArgs a) {
       int nlc = 0;
       for (int l = lane; l < n_real; l += 32) nlc += ((nl[l] & 0x7fff) < consume_to) ? 1 : 0;
       nlc = (int)warp_sum_u64((unsigned long long)nlc);
-      cm_state = (comment_tail && consume_to == hi) ? tile_end_state : S_CODE;
+      cm_state = (comment_tail && consume_to == hi) ? tile_end_state : ((cut >= 0 && consume_to == cut) ? cut_state : S_CODE);
       if (nlc > 0) {
         const unsigned last = nl[nlc - 1];
         if ((int)(last & 0x7fff) == consume_to - 1 && (last & 0x8000)) cm_state = S_BLK;

@@ -79,4 +79,11 @@ EDGE_CASES = {
     "long_trailing_comment": _k("add.s32 %r1, %r2, 1; // " + "y; " * 1700 + "\n @%p1 sub.s32 %r1, %r1, 2; // short\n ret;"),
     "huge_line_comment": "// " + "z{" * 6500 + "\n" + _k("ld.global.f32 %f1, [%rd1]; //" + "/" * 9000 + "\n st.global.f32 [%rd1], %f1;\n ret;"),
     "long_comment_with_block_marks": _k("mov.u32 %r1, 1; // " + "a" * 3000 + " /* " + "b" * 3000 + " */ " + "c" * 3000 + "\n mov.u32 %r2, 2;\n ret;"),
+    # module-level lines longer than a tile in front of the kernel (initialiser lists are emitted on one line), a
+    # one-line parameter list of 9 KB, a 6 KB block comment without a newline, `.entry` decoys inside the long lines
+    "long_const_initialiser": ".version 8.0\n.const .align 4 .b8 table[16384] = {" + ", ".join(str(i % 251) for i in range(16384)) + "};\n"
+                              + ".global .align 1 .b8 $str[9000] = {" + ", ".join("46" for _ in range(9000)) + "};\n" + _k("ld.const.u8 %rs1, [table+5];\n ret;"),
+    "long_param_line": ".visible .entry wide(" + ", ".join(f".param .u64 wide_param_{i}" for i in range(400)) + ") { // {\n add.s32 %r1, %r1, 1;\n ret;\n}\n",
+    "long_block_comment_before": "/* " + "no newline here .entry ghost { " * 200 + "*/ .version 8.0 /* " + "x" * 4200 + " */ " + _k("mov.u32 %r1, 7;\n ret;"),
+    "long_line_then_entry_same_line": ".global .b32 g[3000] = {" + ", ".join("7" for _ in range(3000)) + "}; .visible .entry tail()\n{\n bar.sync 0;\n ret;\n}\n",
 }
