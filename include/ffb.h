@@ -215,7 +215,8 @@ int32_t ffb_skyline(FfbContext* ctx, const double* d_e, const double* d_t, const
  * parse_ptx(source) call (first .entry of the segment, or the one named h_kernel_name).
  *
  * Documented device capacities (status FFB_E_CAPACITY, never a silent difference):
- * a physical line, or a multi-line statement, must fit one 4 KB tile; input is ASCII.
+ * a statement (its code bytes, on one line or several) must fit one 4 KB tile - `//` comments and
+ * module-level lines in front of the kernel body may be of any length; input is ASCII.
  */
 typedef struct {
   uint32_t status;          /* FFB_OK or FFB_E_*  (reference exception of parse_ptx)            */
