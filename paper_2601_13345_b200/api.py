@@ -586,12 +586,47 @@ def pareto_explore(module: PtxModule, cfg: ControlFlowGraph, arch: ArchitectureS
     """explorer.py:186."""
     if not 0 < rho <= 1:
         raise ValueError(f"rho must be in (0, 1], got {rho}")
-    configs = generate_valid_configs(arch, resources, dim_candidates, cap_candidates)
-    if not configs:
+    # Same values as generate_valid_configs -> evaluate_configs -> pareto_front (explorer.py:203-212), without building
+    # the thousands of host objects only to drop most of them: the grid is scored in (block_x, block_y, p_cap) order -
+    # which IS the tie order of explorer.py:113-119 -, ranked on the device, and Prediction objects are made for the
+    # front members alone.
+    caps = sorted(set(cap_candidates)) if cap_candidates else [arch.p_tdp]
+    caps = [float(c) for c in caps if arch.p_cap_min <= c <= arch.p_tdp]
+    spec_row = np.asarray(pack_spec(arch, default_calibration()), dtype=np.float64)
+    shapes = sorted((int(bx), int(by)) for bx, by in engine.enumerate_shapes(spec_row, resources.shared_mem_bytes, dim_candidates))
+    if not shapes or not caps:
         raise NoFeasibleConfig("no candidate configuration passed the hardware filters")
-    predictions = evaluate_configs(module, cfg, arch, profile, resources, configs, jobs=jobs)
-    idx, t_peak = _front_order(predictions, float(rho))
-    return ParetoSet(entries=tuple(predictions[i] for i in idx), rho=rho, t_peak=t_peak)
+    row = _feature_row(module, cfg)
+    r = engine.score_grid(engine.features_tensor([row]),
+                          engine.resources_tensor([[resources.shared_mem_bytes, resources.total_blocks]]),
+                          engine.spec_rows([(arch, profile)]), engine.shape_rows(shapes), np.asarray(caps),
+                          want=("detail",), strict=True)
+    D = _N
+    det_dev = r.detail[0, 0]                                  # [shape][cap][DETAIL_WIDTH]
+    n = len(shapes) * len(caps)
+    d_e = det_dev[:, :, D.D_E_PRED].reshape(-1).contiguous()
+    d_t = det_dev[:, :, D.D_T_EXEC].reshape(-1).contiguous()
+    if not bool((torch.isfinite(d_e) & torch.isfinite(d_t)).all()):
+        # IEEE gives inf / nan where CPython raises (a zero divisor such as ipc = 0, time_model.py:116)
+        raise ZeroDivisionError("float division by zero")
+    rt = native.get_runtime()
+    try:
+        fi, fn, tp = engine.skyline_groups(d_e, d_t, 1, n, rho=float(rho), cap_front=n, rt=rt)
+        idx, t_peak = fi[0, : int(fn.cpu()[0])].cpu().numpy(), float(tp.cpu()[0])
+    except CapacityExceeded:
+        ids, _, _, t_peak = engine.skyline(d_e, d_t, ids=torch.arange(n, dtype=torch.int64, device=d_e.device), rho=float(rho),
+                                           cap_front=n, rt=rt)
+        idx, t_peak = ids.cpu().numpy(), float(t_peak)
+    C = len(caps)
+    rows = det_dev.reshape(n, -1)[torch.from_numpy(np.asarray(idx, dtype=np.int64)).to(det_dev.device)].cpu().numpy().tolist()
+    entries = []
+    for g, d in zip(idx.tolist(), rows):
+        bx, by = shapes[g // C]
+        entries.append(Prediction(LaunchConfig(block_x=bx, block_y=by, p_cap=caps[g % C]),
+                                  TimeBreakdown(d[D.D_MWP], d[D.D_CWP], d[D.D_BW_EFF], d[D.D_T_MEM], d[D.D_T_COMP], d[D.D_T_SYNC], d[D.D_T_EXEC]),
+                                  PowerBreakdown(d[D.D_P_UNITS], d[D.D_P_SHAPE], d[D.D_P_MEM], d[D.D_P_SM], d[D.D_P_DYN], d[D.D_F_ADJ], d[D.D_CI],
+                                                 int(d[D.D_ACTIVE_SMS]), d[D.D_CAP_LIMITED] != 0.0), d[D.D_E_PRED]))
+    return ParetoSet(entries=tuple(entries), rho=rho, t_peak=t_peak)
 
 
 def pareto_explore_sweep(module: PtxModule, cfg: ControlFlowGraph, specs: list, resources: list[InputResources],
