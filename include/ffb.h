@@ -335,6 +335,7 @@ typedef struct {
   uint32_t flags;                 /* FFB_FLOW_* bits                                            */
 } FfbFlowDesc;
 #define FFB_FLOW_SEQUENTIAL_PASS 1u   /* textual pass on one lane only (the general form; default: 32 statements per round) */
+#define FFB_FLOW_ONE_KERNEL 2u        /* CFG + dataflow in one launch (default for feature rows only: two launches) */
 int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, void* stream);
 /* 61-bit name hash the lexer assigns to labels / registers (for annotation keys). */
 uint64_t ffb_name_hash(const uint8_t* name, int64_t len);

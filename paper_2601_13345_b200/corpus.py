@@ -107,6 +107,7 @@ class LexResult:
 LEX_EXACT_ONLY = 1
 LEX_NO_LOCKSTEP = 2
 FLOW_SEQUENTIAL_PASS = 1
+FLOW_ONE_KERNEL = 2
 FLOW_FLAGS_DEFAULT = 0         # FFB_FLOW_* bits for every call (tests flip this)
 LEX_FLAGS_DEFAULT = 0          # extra FFB_LEX_* bits for every call (benchmark A/B switches)
 EXACT_ONLY_DEFAULT = False      # tests flip this to run the exact statement walk alone

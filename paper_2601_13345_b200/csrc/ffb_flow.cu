@@ -38,6 +38,10 @@ constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
 constexpr uint32_t kNoBlock = 0xffffffffu;
 
+// two-kernel form: state of one PTX kernel between the CFG kernel and the dataflow kernel (everything else -
+// block_of, weight - already lives in the context's scratch)
+struct FlowMid { uint32_t status, nb, n_edges, n_loops; };
+
 struct FlowArgs {
   int64_t n_segs;
   const FfbSegInfo* info;
@@ -47,7 +51,8 @@ struct FlowArgs {
   const FfbLabelRec* labels;
   const uint32_t* meta_arr;     // optional compact meta words
   const int32_t* order;
-  unsigned long long* work;     // work-queue counter
+  unsigned long long* work;     // work-queue counters (one per kernel of the two-kernel form)
+  struct FlowMid* mid;          // [K] what the CFG kernel hands to the dataflow kernel
   double default_trip;
   int parallel_pass;            // 0: textual pass on lane 0 only (test switch)
   const uint64_t* ann_hash;     // device copies
@@ -333,30 +338,44 @@ FFB_D double warp_sum_d(double v) {
 // "last match" scans of the trip recogniser, weights, record staging.  Lane 0 alone: the graph
 // walks (DFS, dominators, loop bodies) and the textual dataflow pass, which are sequential by
 // nature.
-__global__ void __launch_bounds__(kFlowWarps * 32, 6)
+// kPart 0: the whole analysis of a PTX kernel in one launch (the drop-in API's detail outputs, annotations).
+// kPart 1 / 2: the same code as two launches - CFG, loops, trips and block weights (no scale maps: a third of the
+// shared memory, more resident warps for its latency-bound scratch walks), then the textual dataflow pass - each
+// half the instruction footprint of the whole.  What crosses the cut is FlowMid + the scratch arrays.
+template <int kPart>
+__global__ void __launch_bounds__(kFlowWarps * 32, kPart == 1 ? 8 : 6)
 flow_kernel(FlowArgs a) {
-  __shared__ uint64_t s_ckey[kFlowWarps][kMapSlots];
-  __shared__ int64_t s_cval[kFlowWarps][kMapSlots];
-  __shared__ uint64_t s_chkey[kFlowWarps][64];      // chunk-local: names the 32 statements in flight define
-  __shared__ uint32_t s_chmask[kFlowWarps][64];     //              ... and the lanes that define them
-  __shared__ int64_t s_chval[kFlowWarps][32];
-  __shared__ uint32_t s_blist[kFlowWarps][kBodyList];   // blocks of the loop being analysed       //              ... and the values they publish
+  constexpr int kMs = kPart == 1 ? 1 : kMapSlots, kCh = kPart == 1 ? 1 : 64;
+  __shared__ uint64_t s_ckey[kFlowWarps][kMs];
+  __shared__ int64_t s_cval[kFlowWarps][kMs];
+  __shared__ uint64_t s_chkey[kFlowWarps][kCh];     // chunk-local: names the 32 statements in flight define
+  __shared__ uint32_t s_chmask[kFlowWarps][kCh];    //              ... and the lanes that define them
+  __shared__ int64_t s_chval[kFlowWarps][kPart == 1 ? 1 : 32];                          //              ... and the values they publish
+  __shared__ uint32_t s_blist[kFlowWarps][kPart == 2 ? 1 : kBodyList];   // blocks of the loop being analysed
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   for (;;) {
     unsigned long long w = 0;
-    if (lane == 0) w = atomicAdd(a.work, 1ull);
+    if (lane == 0) w = atomicAdd(a.work + (kPart == 2 ? 1 : 0), 1ull);
     w = __shfl_sync(kAll, w, 0);
     if (w >= (unsigned long long)a.n_segs) break;
     const int64_t k = a.order ? (int64_t)a.order[w] : (int64_t)w;
     const FfbSegInfo inf = a.info[k];
     double* feat = a.feat + k * FFB_FEAT_WIDTH;
-    if (lane < FFB_FEAT_WIDTH) feat[lane] = lane == FFB_F_OVR_TEXEC ? NAN : 0.0;
+    if (kPart != 2 && lane < FFB_FEAT_WIDTH) feat[lane] = lane == FFB_F_OVR_TEXEC ? NAN : 0.0;
     uint32_t status = inf.status;
     FfbFlowInfo fi;
     fi.n_blocks = fi.n_edges = fi.n_loops = 0; fi.reserved = 0;
-    if (status != FFB_OK) {
-      if (lane == 0) { a.status[k] = status; if (a.flow) a.flow[k] = fi; }
+    uint32_t nb = 0, n_edges = 0, n_loops = 0;
+    if (kPart == 2) {                                // the CFG kernel reported this PTX kernel's status already
+      const FlowMid md = a.mid[k];
+      if (md.status != FFB_OK) continue;
+      nb = md.nb; n_edges = md.n_edges; n_loops = md.n_loops;
+    } else if (status != FFB_OK) {
+      if (lane == 0) {
+        a.status[k] = status; if (a.flow) a.flow[k] = fi;
+        if (kPart == 1) { FlowMid md; md.status = status; md.nb = md.n_edges = md.n_loops = 0; a.mid[k] = md; }
+      }
       continue;
     }
     const uint32_t n = inf.n_instr, L = inf.n_labels;
@@ -386,9 +405,10 @@ flow_kernel(FlowArgs a) {
     st.g.cap = 4; while (st.g.cap < 2 * n + 2) st.g.cap <<= 1;      // <= 4n + 8
     st.ckey = s_ckey[wid]; st.cval = s_cval[wid]; st.used = 0; st.spilled = false;
 
+    if (kPart != 1) for (uint32_t i = lane; i < kMapSlots; i += 32) st.ckey[i] = 0;
+    if (kPart != 2) {                                // ======== CFG, loops, trips, weights ========
     // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
     for (uint32_t i = lane; i < lt.cap; i += 32) { lt.key[i] = 0; lt.first[i] = 0xffffffffu; lt.last[i] = 0; }
-    for (uint32_t i = lane; i < kMapSlots; i += 32) st.ckey[i] = 0;
     for (uint32_t i = lane; i < n; i += 32) block_of[i] = 0;
     __syncwarp();
     for (uint32_t i = lane; i < L; i += 32) {
@@ -415,7 +435,7 @@ flow_kernel(FlowArgs a) {
     }
     if (lane == 0) block_of[0] = 1;
     __syncwarp();
-    uint32_t nb = 0;
+    nb = 0;
     for (uint32_t c = 0; c < n; c += 32) {
       const uint32_t i = c + lane;
       const bool f = i < n && block_of[i] != 0;
@@ -453,11 +473,14 @@ flow_kernel(FlowArgs a) {
       if (t1 >= 0) atomicAdd(&pred_ptr[t1 + 1], 1u);
     }
     if (__any_sync(kAll, bad_target)) {
-      if (lane == 0) { a.status[k] = FFB_E_MALFORMED_PTX; if (a.flow) a.flow[k] = fi; }
+      if (lane == 0) {
+        a.status[k] = FFB_E_MALFORMED_PTX; if (a.flow) a.flow[k] = fi;
+        if (kPart == 1) { FlowMid md; md.status = FFB_E_MALFORMED_PTX; md.nb = md.n_edges = md.n_loops = 0; a.mid[k] = md; }
+      }
       continue;
     }
     __syncwarp();
-    uint32_t n_edges = 0;
+    n_edges = 0;
     {   // inclusive scan of pred_ptr[1..nb] in chunks of 32
       uint32_t carry = 0;
       for (uint32_t c = 1; c <= nb; c += 32) {
@@ -523,7 +546,7 @@ flow_kernel(FlowArgs a) {
     for (uint32_t b = lane; b < nb; b += 32) mark[b] = 0;
     __syncwarp();
     // ---- natural loops, one per header in ascending header order (cfg.py:124-151) ----
-    uint32_t n_loops = 0;
+    n_loops = 0;
     for (uint32_t h = 0; h < nb; ++h) {
       const uint32_t stamp = h + 1;
       int is_header = 0;
@@ -727,6 +750,19 @@ flow_kernel(FlowArgs a) {
       __syncwarp();
     }
     __syncwarp();
+    }                                                // ======== end of the CFG part ========
+    if (kPart == 1) {
+      // trip errors are warp-uniform, but the OR costs nothing; the scratch writes of this warp are ordered
+      // before the next launch by the kernel boundary
+      uint32_t st_all = status;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) st_all |= __shfl_xor_sync(kAll, st_all, d);
+      if (lane == 0) {
+        FlowMid md; md.status = st_all; md.nb = nb; md.n_edges = n_edges; md.n_loops = n_loops; a.mid[k] = md;
+        if (st_all != FFB_OK) { a.status[k] = st_all; if (a.flow) { fi.n_blocks = nb; fi.n_edges = n_edges; fi.n_loops = n_loops; a.flow[k] = fi; } }
+      }
+      continue;
+    }
     // ---- one textual pass: affine scales, aligned fraction, dynamic counts ----
     // Parallel form: 32 statements per round, one per lane.  A chunk-local table maps every register
     // the chunk defines to the mask of defining lanes, so a source is either "before the chunk" (looked
@@ -951,7 +987,7 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
                o_mk = take(n1, 4), o_sk = take(n1, 4), o_w = take(n1, 8), o_lk = take(nL, 8), o_lf = take(nL, 4),
                o_ll = take(nL, 4), o_sk2 = take(nS, 8), o_sv = take(nS, 8),
                o_ah = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8), o_at = take((size_t)(d->n_ann > 0 ? d->n_ann : 1), 8),
-               o_work = take(2, 8);
+               o_work = take(2, 8), o_mid = take((size_t)K, sizeof(FlowMid));
   int32_t rc = ffb_reserve(ctx, &ctx->d_flow, bytes);
   if (rc) return rc;
   char* base = (char*)ctx->d_flow.p;
@@ -972,7 +1008,8 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   a.sc_key = (uint64_t*)(base + o_sk2); a.sc_val = (int64_t*)(base + o_sv);
   a.ann_hash = (const uint64_t*)(base + o_ah); a.ann_trip = (const double*)(base + o_at);
   a.work = (unsigned long long*)(base + o_work);
-  FFB_CUDA(ctx, cudaMemsetAsync(a.work, 0, 8, stream));
+  a.mid = (FlowMid*)(base + o_mid);
+  FFB_CUDA(ctx, cudaMemsetAsync(a.work, 0, 16, stream));
   if (a.n_ann > 0) {
     if (!d->h_ann_hash || !d->h_ann_trip) return ffb_fail(ctx, FFB_E_BAD_ARGUMENT, "ffb_kernel_features: annotation arrays missing");
     rc = ffb_stage_reserve(ctx, (size_t)a.n_ann * 16);
@@ -989,8 +1026,16 @@ extern "C" int32_t ffb_kernel_features(FfbContext* ctx, const FfbFlowDesc* d, vo
   int64_t ctas = (K + kFlowWarps - 1) / kFlowWarps;
   const int64_t max_ctas = (int64_t)ctx->sm_count * 16;
   if (ctas > max_ctas) ctas = max_ctas;
-  FFB_LAUNCH(flow_kernel, (unsigned)ctas, kFlowWarps * 32, 0, stream, a);
-  return ffb_check_launch(ctx, "flow_kernel");
+  const bool detail = d->d_flow || d->d_block_start || d->d_edges || d->d_loops || d->d_loop_body || d->d_weights || a.n_ann > 0;
+  if (detail || (d->flags & FFB_FLOW_ONE_KERNEL)) {
+    FFB_LAUNCH(flow_kernel<0>, (unsigned)ctas, kFlowWarps * 32, 0, stream, a);
+    return ffb_check_launch(ctx, "flow_kernel");
+  }
+  FFB_LAUNCH(flow_kernel<1>, (unsigned)ctas, kFlowWarps * 32, 0, stream, a);
+  rc = ffb_check_launch(ctx, "flow_kernel<cfg>");
+  if (rc) return rc;
+  FFB_LAUNCH(flow_kernel<2>, (unsigned)ctas, kFlowWarps * 32, 0, stream, a);
+  return ffb_check_launch(ctx, "flow_kernel<dataflow>");
 }
 
 // Name hash used for annotation keys (same function as the lexer's label hash).

@@ -316,6 +316,14 @@ def test_parallel_textual_pass_equals_sequential(backend):
         assert np.array_equal(par.status.cpu().numpy(), seq.status.cpu().numpy())
         ok = par.status.cpu().numpy() == 0
         assert par.feat.cpu().numpy()[ok, :11].tobytes() == seq.feat.cpu().numpy()[ok, :11].tobytes()
+        # the default form is two launches (CFG / trips / weights, then the dataflow pass); one launch gives the same rows
+        corpus.FLOW_FLAGS_DEFAULT = corpus.FLOW_ONE_KERNEL
+        try:
+            one = corpus.kernel_features(corp, lex)
+        finally:
+            corpus.FLOW_FLAGS_DEFAULT = 0
+        assert np.array_equal(par.status.cpu().numpy(), one.status.cpu().numpy())
+        assert par.feat.cpu().numpy()[ok, :11].tobytes() == one.feat.cpu().numpy()[ok, :11].tobytes()
 
 
 def test_segment_range_calls_equal_whole_corpus(backend):
