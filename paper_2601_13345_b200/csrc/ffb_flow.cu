@@ -8,6 +8,8 @@
 // %tid.x scale map, single textual pass) and :128-147 (weighted aligned fraction),
 // features.py:62-81 (dynamic counts).
 //
+// Launched as TWO kernels for feature rows (flow_kernel<1>: CFG, loops, trips, weights; flow_kernel<2>: the textual
+// dataflow pass) and as one (flow_kernel<0>) when the caller wants the detail outputs; see the template's comment.
 // One WARP per kernel (dynamic queue, longest first).  Lane-parallel: label table, leaders, block
 // numbering, edges, predecessor lists, the "last match" scans of the trip recogniser, weights and
 // the textual dataflow pass (32 statements per round).  Lane 0 alone: DFS, dominators and loop
