@@ -663,7 +663,7 @@ extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* st
     // measured: record mode 17.1 ms vs 32.0 ms per 1.44 GB (r1p); histogram mode 482 vs 416 GB/s once its
     // parser had been shortened (r1z; before that the barrier cost it 3%)
     const bool lockstep = !(d->flags & FFB_LEX_NO_LOCKSTEP);
-    const int fwarps = lockstep ? (records ? 16 : 24) : kFWarps;
+    const int fwarps = lockstep ? (records ? kFRecLockWarps : 24) : kFWarps;
     const size_t fsmem = (size_t)fwarps * (records ? kFWarpSmemRec : kFWarpSmemHist);
     int64_t fctas = (d->n_segs + fwarps - 1) / fwarps;
     const int64_t fmax = lockstep ? (int64_t)ctx->sm_count : (int64_t)ctx->sm_count * (records ? 4 : 6);

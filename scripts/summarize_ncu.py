@@ -19,9 +19,9 @@ def raw(rep: Path):
     txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     if len(rows) < 3:
-        return {}
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+        return []
+    hdr, units = rows[0], rows[1]
+    return [{h: (v, u) for h, u, v in zip(hdr, units, vals)} for vals in rows[2:] if len(vals) == len(hdr)]   # one per captured launch
 
 
 def main(tag: str):
@@ -29,9 +29,7 @@ def main(tag: str):
     lines = [f"# ncu --set full summaries ({tag}); one launch per kernel, cold cache, --clock-control none"]
     traffic = {}
     for rep in sorted((ROOT / "gpurun_out").glob(f"prof_*_{tag}.ncu-rep")):
-        m = raw(rep)
-        if not m:
-            continue
+      for m in raw(rep):
         name = m.get("Kernel Name", ("?", ""))[0]
         lines.append(f"\n## {rep.name}: {name}")
         for w in WANT:
@@ -45,7 +43,8 @@ def main(tag: str):
         dur, du = m.get("gpu__time_duration.sum", ("0", "ns"))
         dur_s = float(dur.replace(",", "")) * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}.get(du, 1e-9)
         lines.append(f"{'dram traffic (read+write)':70s} {tr/1e6:16.3f} MB  -> {tr/1e9/max(dur_s,1e-12):.1f} GB/s over {dur_s*1e3:.3f} ms")
-        key = name.split('(')[0].split('::')[-1].split('<')[0]
+        base = name.split('(')[0].split('::')[-1]
+        key = base if base.startswith('flow_kernel<') else base.split('<')[0]          # flow_kernel<1> / <2> are two kernels
         traffic[key + ('_hist' if '_hist_' in rep.name else '')] = tr
     (OUT / f"ncu_full_{tag}.txt").write_text("\n".join(lines) + "\n")
     # launch list
