@@ -35,6 +35,7 @@ namespace {
 constexpr int kFlowWarps = 4;
 constexpr int kMapSlots = 512;                    // shared-memory register -> scale map per warp (8 KB)
 constexpr int kMapFill = 384;
+constexpr int kLeadWords = 256;                   // flow_kernel<1>: leader flags of kernels up to 8 192 statements as a shared-memory bit set
 constexpr int kBodyList = 32;                     // loop bodies up to this many blocks are scanned through a compact list                     // entries kept on chip; later names spill to the HBM table
 constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
@@ -354,6 +355,7 @@ flow_kernel(FlowArgs a) {
   __shared__ uint32_t s_chmask[kFlowWarps][kCh];    //              ... and the lanes that define them
   __shared__ int64_t s_chval[kFlowWarps][kPart == 1 ? 1 : 32];                          //              ... and the values they publish
   __shared__ uint32_t s_blist[kFlowWarps][kPart == 2 ? 1 : kBodyList];   // blocks of the loop being analysed
+  __shared__ uint32_t s_lead[kFlowWarps][kPart == 1 ? kLeadWords : 1];   // leader flags (labels), one bit per statement
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   for (;;) {
@@ -411,7 +413,13 @@ flow_kernel(FlowArgs a) {
     if (kPart != 2) {                                // ======== CFG, loops, trips, weights ========
     // ---- labels: last definition wins, dictionary order = first definition (ptx.py:234) ----
     for (uint32_t i = lane; i < lt.cap; i += 32) { lt.key[i] = 0; lt.first[i] = 0xffffffffu; lt.last[i] = 0; }
-    for (uint32_t i = lane; i < n; i += 32) block_of[i] = 0;
+    // flow_kernel<1>, up to 32 * kLeadWords statements: the leader flags live in a shared-memory bit set and the
+    // statements are visited once (meta word in, block number out) instead of a zero fill, two flag passes and a
+    // read-back of block_of in HBM
+    const bool lead_bits = kPart == 1 && n <= 32u * (uint32_t)kLeadWords;
+    uint32_t* lbits = s_lead[wid];
+    if (lead_bits) { for (uint32_t i = lane; i < (n + 31u) / 32u; i += 32) lbits[i] = 0; }
+    else { for (uint32_t i = lane; i < n; i += 32) block_of[i] = 0; }
     __syncwarp();
     for (uint32_t i = lane; i < L; i += 32) {
       const uint64_t key = lab[i].hash + 1;
@@ -428,16 +436,47 @@ flow_kernel(FlowArgs a) {
     // ---- leaders (cfg.py:63-70); block_of doubles as the flag array first ----
     for (uint32_t i = lane; i < L; i += 32) {
       const uint32_t s = lt.find(lab[i].hash);
-      if (lt.last[s] == i && lab[i].index < n) block_of[lab[i].index] = 1;     // effective definition only
+      if (lt.last[s] == i && lab[i].index < n) {                               // effective definition only
+        const uint32_t at = lab[i].index;
+        if (lead_bits) atomicOr(&lbits[at >> 5], 1u << (at & 31u)); else block_of[at] = 1;
+      }
     }
-    for (uint32_t i = lane; i + 1 < n; i += 32) {
-      const uint32_t m = FFB_META(i);
-      const uint32_t base = ffb_meta_base(m);
-      if (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT) block_of[i + 1] = 1;
+    if (!lead_bits) {
+      for (uint32_t i = lane; i + 1 < n; i += 32) {
+        const uint32_t m = FFB_META(i);
+        const uint32_t base = ffb_meta_base(m);
+        if (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT) block_of[i + 1] = 1;
+      }
+      if (lane == 0) block_of[0] = 1;
     }
-    if (lane == 0) block_of[0] = 1;
     __syncwarp();
     nb = 0;
+    if (lead_bits) {
+      // four chunks of 32 statements per trip: the four meta loads are in flight together
+      unsigned carry = 1u;                           // statement 0 is a leader; then: the previous chunk ended in a branch / ret / exit
+      for (uint32_t c = 0; c < n; c += 128) {
+        uint32_t m4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { const uint32_t i = c + 32u * u + lane; m4[u] = i < n ? FFB_META(i) : 0u; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t cc = c + 32u * u;
+          if (cc < n) {                              // warp-uniform
+            const uint32_t i = cc + lane;
+            const uint32_t m = m4[u], base = ffb_meta_base(m);
+            const bool ends = i < n && (ffb_meta_cls(m) == FFB_CLS_BRANCH || base == FFB_BASE_RET || base == FFB_BASE_EXIT);
+            const unsigned em = __ballot_sync(kAll, ends);
+            unsigned lead = lbits[cc >> 5] | (em << 1) | carry;
+            carry = em >> 31;
+            if (n - cc < 32u) lead &= (1u << (n - cc)) - 1u;
+            const uint32_t id = nb + __popc(lead & (0xffffffffu >> (31 - lane))) - 1;   // leaders at or before me
+            if (i < n) block_of[i] = id;
+            if ((lead >> lane) & 1u) block_start[id] = i;
+            nb += __popc(lead);
+          }
+        }
+      }
+    } else
     for (uint32_t c = 0; c < n; c += 32) {
       const uint32_t i = c + lane;
       const bool f = i < n && block_of[i] != 0;
