@@ -435,3 +435,46 @@ def test_loop_body_larger_than_the_block_list(backend):
         lines += [f"\tsetp.lt.s32 %p2, %r2, {i};", f"\t@%p2 bra S{i};", "\tadd.s32 %r3, %r3, 1;", f"S{i}:", "\tmul.lo.s32 %r4, %r3, 3;"]
     lines += ["\tadd.s32 %r1, %r1, 1;", "\tsetp.lt.s32 %p1, %r1, 10;", "\t@%p1 bra LOOP;", "\tret;", "}", ""]
     _check(["\n".join(lines)])
+
+
+def _chunk_edge_kernel(name: str, n_stmt: int, branch_at: tuple[int, ...], label_at: tuple[int, ...]) -> str:
+    """``n_stmt`` statements; a predicated forward branch at each index of ``branch_at`` and a label in front of each
+    statement of ``label_at`` (indices count instructions, as K1b's block numbering does)."""
+    lines = [f".visible .entry {name}(.param .u64 p0)", "{", "\t.reg .b32 %r<9>;", "\t.reg .pred %p<4>;"]
+    for i in range(n_stmt - 1):
+        if i in label_at:
+            lines.append(f"T{i}:")
+        if i in branch_at:
+            lines.append("\t@%p1 bra DONE;")
+        else:
+            lines.append(f"\tadd.s32 %r{1 + i % 7}, %r{1 + (i + 3) % 7}, {i % 11};")
+    lines += ["DONE:", "\tret;", "}", ""]
+    return "\n".join(lines)
+
+
+def test_leader_pass_chunk_edges_and_fallback(backend):
+    """flow_kernel<1> numbers the blocks in one visit per statement: leader flags of labels in a shared-memory bit set,
+    branch flags as the chunk's ballot shifted by one with a carry into the next chunk of 32, four chunks per trip;
+    kernels above 8 192 statements take the flag-array form.  Branches on the last lane of a chunk / of a trip, labels on
+    the first, statement counts around 32, 128 and 8 192: rows equal the oracle's and the one-launch kernel's."""
+    sizes = [1, 2, 31, 32, 33, 64, 127, 128, 129, 160, 257]
+    big = [8191, 8192, 8193] if backend == "emul" else [8191, 8192, 8193, 12000]
+    texts = []
+    for j, n in enumerate(sizes + big):
+        edges = tuple(i for i in (30, 31, 32, 63, 95, 126, 127, 128, 255, 8190, 8191) if i < n - 1)
+        labs = tuple(i for i in (0, 1, 32, 64, 127, 128, 129, 256, 8191, 8192) if i < n - 1)
+        texts.append(_chunk_edge_kernel(f"edge{j}", n, edges, labs))
+    _check(texts[:len(sizes)])
+    corp = _corpus(texts)
+    lex = corpus.lex_records(corp)
+    two = corpus.kernel_features(corp, lex)
+    corpus.FLOW_FLAGS_DEFAULT = corpus.FLOW_ONE_KERNEL
+    try:
+        one = corpus.kernel_features(corp, lex)
+    finally:
+        corpus.FLOW_FLAGS_DEFAULT = 0
+    assert not two.status.cpu().numpy().any() and not one.status.cpu().numpy().any()
+    assert two.feat.cpu().numpy()[:, :11].tobytes() == one.feat.cpu().numpy()[:, :11].tobytes()
+    k = len(sizes)                                     # the smallest of the large kernels against the oracle as well
+    want = np.asarray(orc.kernel_feature_row(texts[k]), dtype=np.float64)
+    assert two.feat.cpu().numpy()[k, :11].tobytes() == want.tobytes()
