@@ -666,7 +666,7 @@ extern "C" int32_t ffb_lex_corpus(FfbContext* ctx, const FfbLexDesc* d, void* st
     const int fwarps = lockstep ? (records ? kFRecLockWarps : 24) : kFWarps;
     const size_t fsmem = (size_t)fwarps * (records ? kFWarpSmemRec : kFWarpSmemHist);
     int64_t fctas = (d->n_segs + fwarps - 1) / fwarps;
-    const int64_t fmax = lockstep ? (int64_t)ctx->sm_count : (int64_t)ctx->sm_count * (records ? 4 : 6);
+    const int64_t fmax = lockstep ? (int64_t)ctx->sm_count * (records ? kFRecCtasPerSm : 1) : (int64_t)ctx->sm_count * (records ? 4 : 6);
     if (fctas > fmax) fctas = fmax;
 #define FFB_LAUNCH_FAST(R, L)                                                                                          \
     do {                                                                                                               \

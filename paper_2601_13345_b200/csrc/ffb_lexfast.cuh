@@ -47,7 +47,11 @@ namespace {
 #endif
 constexpr bool kPrefetch = FFB_LEX_PREFETCH != 0;
 constexpr int kFWarps = 4;
-constexpr int kFRecLockWarps = 16;               // warps of the barrier-paced record-mode CTA (one CTA per SM)
+#ifndef FFB_LEX_REC_CTAS
+#define FFB_LEX_REC_CTAS 1                       // barrier-paced record-mode CTAs per SM (16 warps per SM in all)
+#endif
+constexpr int kFRecCtasPerSm = FFB_LEX_REC_CTAS;
+constexpr int kFRecLockWarps = 16 / kFRecCtasPerSm;   // warps of the barrier-paced record-mode CTA
 constexpr int kFTile = 4096;
 constexpr int kFPad = 64;
 constexpr int kFWords = kFTile / 32;              // 32-byte mask words per tile
@@ -746,7 +750,7 @@ FFB_D bool in_line_comment(const uint8_t* s, int at, int lo) {   // is a "//" op
 // instruction lines; without it 70% of the issue slots of the record-mode kernel waited for
 // instruction fetch (ncu r1o).
 template <bool kRecords, bool kLockstep>
-__global__ void __launch_bounds__(kLockstep ? (kRecords ? kFRecLockWarps * 32 : 768) : kFWarps * 32, kLockstep ? 1 : (kRecords ? 4 : 6))
+__global__ void __launch_bounds__(kLockstep ? (kRecords ? kFRecLockWarps * 32 : 768) : kFWarps * 32, kLockstep ? (kRecords ? kFRecCtasPerSm : 1) : (kRecords ? 4 : 6))
 lex_fast_kernel(LexArgs a) {
   constexpr int kMain = kRecords ? 2 : 1;
   FFB_DYN_SMEM(smem_raw);
