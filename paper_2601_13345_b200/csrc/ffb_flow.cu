@@ -36,6 +36,7 @@ constexpr int kFlowWarps = 4;
 constexpr int kMapSlots = 512;                    // shared-memory register -> scale map per warp (8 KB)
 constexpr int kMapFill = 384;
 constexpr int kLeadWords = 256;                   // flow_kernel<1>: leader flags of kernels up to 8 192 statements as a shared-memory bit set
+constexpr int kLabSlots = 128;                    // flow_kernel<1>: label tables of up to this many slots (<= 63 labels) in shared memory
 constexpr int kBodyList = 32;                     // loop bodies up to this many blocks are scanned through a compact list                     // entries kept on chip; later names spill to the HBM table
 constexpr int64_t kNoneScale = INT64_MIN;            // alignment.py "None"
 constexpr int64_t kBigScale = INT64_MIN + 1;         // |scale| beyond 2^62: known, never aligned
@@ -356,6 +357,9 @@ flow_kernel(FlowArgs a) {
   __shared__ int64_t s_chval[kFlowWarps][kPart == 1 ? 1 : 32];                          //              ... and the values they publish
   __shared__ uint32_t s_blist[kFlowWarps][kPart == 2 ? 1 : kBodyList];   // blocks of the loop being analysed
   __shared__ uint32_t s_lead[kFlowWarps][kPart == 1 ? kLeadWords : 1];   // leader flags (labels), one bit per statement
+  __shared__ uint64_t s_lkey[kFlowWarps][kPart == 1 ? kLabSlots : 1];    // small label tables (2 KB per warp)
+  __shared__ uint32_t s_lfirst[kFlowWarps][kPart == 1 ? kLabSlots : 1];
+  __shared__ uint32_t s_llast[kFlowWarps][kPart == 1 ? kLabSlots : 1];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   for (;;) {
@@ -404,6 +408,9 @@ flow_kernel(FlowArgs a) {
     LabelTable lt;
     lt.key = a.lab_key + 4 * lb + 8 * k; lt.first = a.lab_first + 4 * lb + 8 * k; lt.last = a.lab_last + 4 * lb + 8 * k;
     lt.cap = 4; while (lt.cap < 2 * L + 2) lt.cap <<= 1;          // <= 4L + 8
+    if (kPart == 1 && lt.cap <= (uint32_t)kLabSlots) {             // probed once per label, branch and loop: keep it on chip
+      lt.key = s_lkey[wid]; lt.first = s_lfirst[wid]; lt.last = s_llast[wid];
+    }
     CachedScales st;
     st.g.key = a.sc_key + 4 * ib + 8 * k; st.g.val = a.sc_val + 4 * ib + 8 * k;
     st.g.cap = 4; while (st.g.cap < 2 * n + 2) st.g.cap <<= 1;      // <= 4n + 8
